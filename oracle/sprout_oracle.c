@@ -1,0 +1,533 @@
+/*
+ * sprout_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of the Sprout hot path
+ * (arXiv 2403.12900): quality floor (Eq. 3), expected-carbon cost vector
+ * (Eq. 2 + PUE), the directive LP (Eqs. 4-7) solved by enumerating the
+ * vertices of its feasible polytope, inverse-CDF directive selection from the
+ * solved mix, and per-request carbon accounting (Eq. 1) summed sequentially.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header,
+ * table or constant generator with the CUDA path in paper_2403_12900_b200/.
+ *
+ * Citations: P:<line> = /root/reference/PAPER.md line, S:<line> = SPEC.md
+ * line (SPEC binds only its own CPU program; used for worked examples).
+ * Every reading of a silent/ambiguous passage is listed in DESIGN.md
+ * ("Readings"), named L1..L16 as in SURVEY.md section 8(c).
+ *
+ * Build: gcc -O2 -std=c11 -fPIC -shared -ffp-contract=off -fno-fast-math -pthread
+ * (-ffp-contract=off: no FMA contraction, reading L7.)
+ *
+ * Parity status: every function below is pinned by tests in tests/ against
+ * something other than itself (Random123 known-answer vectors, the paper's
+ * and SPEC's worked examples, exact-rational vertex brute force, SciPy HiGHS
+ * dual simplex, a simplex grid, closed forms and invariants).  None is
+ * "parity unpinned".
+ */
+#include <math.h>
+#include <float.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+#define ORC_MAX_LEVELS 8
+#define ORC_MAX_CLASSES 4
+
+/* ------------------------------------------------------------------------ */
+/* Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11 "Parallel random numbers:
+ * as easy as 1, 2, 3"; the Random123 reference constants).  The paper only
+ * says x_i is "the probability of applying the i-th directive level"
+ * (P:181); the counter-based mechanism is reading L10.                       */
+void orc_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4])
+{
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) {                 /* key schedule: bump before rounds 2..10 */
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t prod0 = (uint64_t)0xD2511F53u * (uint64_t)c0;
+        uint64_t prod1 = (uint64_t)0xCD9E8D57u * (uint64_t)c2;
+        uint32_t hi0 = (uint32_t)(prod0 >> 32), lo0 = (uint32_t)prod0;
+        uint32_t hi1 = (uint32_t)(prod1 >> 32), lo1 = (uint32_t)prod1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* The selection draw of global request g (reading L10):
+ * key = (seed lo32, seed hi32); counter = (g>>2 lo32, g>>2 hi32, 0, 0)
+ * (stream 0 = selection); request g takes output word g & 3.                */
+uint32_t orc_draw_word(uint64_t seed, uint64_t g)
+{
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint64_t blk = g >> 2;
+    uint32_t ctr[4] = { (uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u };
+    uint32_t out[4];
+    orc_philox4x32_10(ctr, key, out);
+    return out[g & 3u];
+}
+
+/* ------------------------------------------------------------------------ */
+/* Eq. 3: q_lb = (1 - (k0 - k0min)/(k0max - k0min) * xi) * q0.
+ * Reading L3: the fraction is clamped to [0,1] and defined as 0 when
+ * k0max <= k0min.  Evaluation order (reading L7): f = (k0-kmin)/(kmax-kmin);
+ * clamp; t = f*xi; u = 1 - t; b = u*q0.                                      */
+double orc_quality_lower_bound(double k0, double kmin, double kmax, double xi, double q0)
+{
+    double f;
+    if (kmax > kmin) {
+        f = (k0 - kmin) / (kmax - kmin);
+        if (f < 0.0) f = 0.0;
+        if (f > 1.0) f = 1.0;
+    } else {
+        f = 0.0;
+    }
+    double t = f * xi;
+    double u = 1.0 - t;
+    return u * q0;
+}
+
+/* Eq. 2 with the PUE multiplier of P:153 on the operational term
+ * (reading L2): c_i = (k0*PUE)*e_i + k1*p_i, the expected gCO2 of one request
+ * at level i (Eq. 1, with E = e_i, T = p_i).                        */
+void orc_cost_vector(int n, double k0, double pue, double k1,
+                     const double *e, const double *p, double *c)
+{
+    double kp = k0 * pue;
+    for (int i = 0; i < n; ++i) {
+        double op = kp * e[i];
+        double em = k1 * p[i];
+        c[i] = op + em;
+    }
+}
+
+/* Eq. 1 for one request: C = CI*PUE*E + (CO2_embed/T_life)*T.
+ * kp = k0*PUE is computed by the caller once per interval.                  */
+double orc_request_carbon(double kp, double k1, double energy_kwh, double time_s)
+{
+    double op = kp * energy_kwh;
+    double em = k1 * time_s;
+    return op + em;
+}
+
+/* ------------------------------------------------------------------------ */
+/* The LP of Eqs. 4-7:  min c.x  s.t.  q.x >= b, 0 <= x_i <= 1,
+ * sum x = 1.  The feasible set is the unit simplex cut by one half-space, so
+ * its vertices are (i) the pure levels e_i with q_i >= b and (ii) for every
+ * pair i<j whose q strictly straddles b, the point on edge (e_i, e_j) where
+ * q.x = b.  An LP attains its minimum at a vertex, so enumerating them in a
+ * fixed order and keeping the first strict minimum IS the LP solution with
+ * a fixed tie-break (readings L6, L8).  Edge arithmetic, reading L7:
+ *   h = higher-q end, l = lower-q end; kept only if c_l < c_h (otherwise the
+ *   pure vertex h, enumerated earlier, is at least as cheap);
+ *   x_h = (b - q_l)/(q_h - q_l);  x_l = 1 - x_h;  obj = c_l + (c_h - c_l)*x_h.
+ * Vertex ids: pure i -> i; edge (i,j) -> n + (lexicographic index of (i,j)).
+ * Returns 0 (ok) or 2 (infeasible: no vertex; impossible when b <= q0).     */
+int orc_solve_lp(int n, const double *c, const double *q, double b,
+                 double *x, double *obj, int *vertex)
+{
+    double best = INFINITY;
+    int best_id = -1, best_i = -1, best_j = -1;
+    double best_xi = 0.0, best_xj = 0.0;
+
+    for (int i = 0; i < n; ++i) {                  /* pure vertices, ascending */
+        if (q[i] >= b) {
+            if (c[i] < best) {
+                best = c[i]; best_id = i; best_i = i; best_j = -1;
+            }
+        }
+    }
+    int edge_id = 0;
+    for (int i = 0; i < n; ++i) {                  /* edges, lexicographic */
+        for (int j = i + 1; j < n; ++j, ++edge_id) {
+            int straddle = (q[i] < b && q[j] > b) || (q[i] > b && q[j] < b);
+            if (!straddle) continue;
+            int h = (q[i] > q[j]) ? i : j;
+            int l = (h == i) ? j : i;
+            if (!(c[l] < c[h])) continue;
+            double xh = (b - q[l]) / (q[h] - q[l]);
+            double xl = 1.0 - xh;
+            double o = c[l] + (c[h] - c[l]) * xh;
+            if (o < best) {
+                best = o; best_id = n + edge_id;
+                best_i = h; best_j = l; best_xi = xh; best_xj = xl;
+            }
+        }
+    }
+    if (best_id < 0) {
+        for (int i = 0; i < n; ++i) x[i] = NAN;
+        *obj = NAN;
+        *vertex = 255;
+        return 2;
+    }
+    for (int i = 0; i < n; ++i) x[i] = 0.0;
+    if (best_j < 0) {
+        x[best_i] = 1.0;
+    } else {
+        x[best_i] = best_xi;
+        x[best_j] = best_xj;
+    }
+    *obj = best;
+    *vertex = best_id;
+    return 0;
+}
+
+/* Inverse-CDF thresholds of the solved mix ("probability of selecting
+ * each directive level"; reading L10): cum_i = sum_{k<=i} x_k added
+ * sequentially in fp64, T_i = min(ceil(cum_i * 2^32), 2^32) for i <= n-2,
+ * max_level = first i with T_i = 2^32, else n-1.  T is returned unsaturated
+ * as uint64 (value up to 2^32).                                             */
+void orc_thresholds(int n, const double *x, uint64_t *T, int *max_level)
+{
+    double cum = 0.0;
+    int ml = n - 1, found = 0;
+    for (int i = 0; i + 1 < n; ++i) {
+        cum = cum + x[i];
+        double scaled = ldexp(cum, 32);           /* exact: power-of-two scale */
+        double cl = ceil(scaled);
+        uint64_t t = (cl >= 4294967296.0) ? (uint64_t)4294967296ull : (uint64_t)cl;
+        T[i] = t;
+        if (t == 4294967296ull && !found) { ml = i; found = 1; }
+    }
+    *max_level = ml;
+}
+
+/* Directive selector (P:162 selector (1)), the plain
+ * inverse-CDF definition: with u = w * 2^-32, the level is the smallest
+ * i <= n-2 with u < cum_i, else n-1.  A pinned (opted-out) user always gets
+ * L0.                                                    */
+int orc_select_level(int n, const double *x, uint32_t w, int pinned)
+{
+    if (pinned) return 0;
+    double u = ldexp((double)w, -32);
+    double cum = 0.0;
+    for (int i = 0; i + 1 < n; ++i) {
+        cum = cum + x[i];
+        if (u < cum) return i;
+    }
+    return n - 1;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Per-cell input validation (SURVEY 8(b) cell_status code 1).               */
+static int finite_nonneg(double v) { return v >= 0.0 && v <= DBL_MAX; }
+
+static int cell_inputs_valid(int n, double k0, double kmin, double kmax, double xi,
+                             const double *e, const double *p, const double *q)
+{
+    if (!(xi >= 0.0 && xi <= 1.0)) return 0;
+    if (!finite_nonneg(k0) || !finite_nonneg(kmin) || !finite_nonneg(kmax)) return 0;
+    if (!(kmax >= kmin)) return 0;
+    for (int i = 0; i < n; ++i) {
+        if (!(q[i] >= 0.0 && q[i] <= 1.0)) return 0;
+        if (!finite_nonneg(e[i]) || !finite_nonneg(p[i])) return 0;
+    }
+    return 1;
+}
+
+typedef struct {
+    int n, R, X, ppi, n_classes;
+    int64_t T;
+    const double *k0, *kmin, *kmax, *xi, *e, *p, *q;
+    double k1, pue;
+} orc_problem;
+
+static const double *prof(const orc_problem *P, const double *base, int64_t seg)
+{
+    int64_t row = P->ppi ? seg : seg / P->T;
+    return base + row * P->n;
+}
+
+/* One LP cell (segment seg = r*T + t, quality coefficient index j).
+ * Returns the cell status: 0 ok, 1 invalid input, 2 infeasible.             */
+static int solve_cell(const orc_problem *P, int64_t seg, int j,
+                      double *x, double *obj, double *qlb, int *vertex,
+                      uint64_t *T, int *max_level)
+{
+    int n = P->n;
+    int64_t r = seg / P->T;
+    double k0 = P->k0[seg], kmin = P->kmin[r], kmax = P->kmax[r], xi = P->xi[j];
+    const double *e = prof(P, P->e, seg), *p = prof(P, P->p, seg), *q = prof(P, P->q, seg);
+    if (!cell_inputs_valid(n, k0, kmin, kmax, xi, e, p, q)) {
+        for (int i = 0; i < n; ++i) x[i] = NAN;
+        *obj = NAN; *qlb = NAN; *vertex = 255;
+        for (int i = 0; i + 1 < n; ++i) T[i] = 4294967296ull;
+        *max_level = 0;
+        return 1;
+    }
+    double b = orc_quality_lower_bound(k0, kmin, kmax, xi, q[0]);
+    double c[ORC_MAX_LEVELS];
+    orc_cost_vector(n, k0, P->pue, P->k1, e, p, c);
+    *qlb = b;
+    int st = orc_solve_lp(n, c, q, b, x, obj, vertex);
+    if (st != 0) {
+        for (int i = 0; i + 1 < n; ++i) T[i] = 4294967296ull;
+        *max_level = 0;
+        return st;
+    }
+    orc_thresholds(n, x, T, max_level);
+    return 0;
+}
+
+/* All cells of segments [first_segment, first_segment + n_segments), cell
+ * index (s - first_segment)*X + j (reading: xi innermost, SURVEY 8 notation).
+ * Returns 0, or 1 on invalid scalar arguments.                              */
+int orc_solve_cells(int n, int R, int64_t T, int X,
+                    const double *k0, const double *kmin, const double *kmax, const double *xi,
+                    const double *e, const double *p, const double *q, int profile_per_interval,
+                    double k1, double pue, int64_t first_segment, int64_t n_segments,
+                    double *x, double *objective, double *q_lb, uint8_t *vertex,
+                    uint64_t *threshold, uint8_t *max_level, uint8_t *cell_status)
+{
+    if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1) return 1;
+    if (!(pue >= 1.0 && pue <= DBL_MAX) || !(k1 >= 0.0 && k1 <= DBL_MAX)) return 1;
+    if (first_segment < 0 || n_segments < 0 || first_segment + n_segments > (int64_t)R * T) return 1;
+    orc_problem P = { n, R, X, profile_per_interval, 1, T, k0, kmin, kmax, xi, e, p, q, k1, pue };
+    for (int64_t s = 0; s < n_segments; ++s) {
+        for (int j = 0; j < X; ++j) {
+            int64_t cell = s * X + j;
+            int vid, ml;
+            uint64_t Tl[ORC_MAX_LEVELS];
+            int st = solve_cell(&P, first_segment + s, j, x + cell * n, objective + cell,
+                                q_lb + cell, &vid, Tl, &ml);
+            vertex[cell] = (uint8_t)vid;
+            max_level[cell] = (uint8_t)ml;
+            cell_status[cell] = (uint8_t)st;
+            for (int i = 0; i + 1 < n; ++i) threshold[cell * (n - 1) + i] = Tl[i];
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Trace replay of selected segments.  For every request of a segment, in
+ * index order: draw w (L10), read pinned/class flags (reading L11),
+ * and for every cell of the segment select the level, evaluate the
+ * request's energy E = ef + et*tok and time T = pf + pt*tok (P:87-98 linear
+ * in generated tokens; reading L11), its carbon C = (k0*PUE)*E + k1*T
+ * (Eq. 1, reading L2), and add to the cell's running fp64 sums in
+ * request order (reading L16).  Also: integer counts and token sums per
+ * (cell, class, level), the per-segment Base counterfactual (all requests at
+ * L0), and the realised quality sum q[level] (reading L15).   */
+typedef struct {
+    const orc_problem *P;
+    uint64_t seed;
+    const double *ef, *et, *pf, *pt;   /* [4][8] */
+    const int64_t *seg_id, *req_begin, *seg_m;
+    const uint64_t *g0;
+    const uint16_t *tokens; int64_t pitch;
+    const uint8_t *flags;
+    uint64_t *cnt, *tok;
+    double *energy, *time_s, *carbon, *quality;
+    uint64_t *seg_count, *seg_pinned, *seg_tok;
+    double *seg_base;
+    uint8_t *levels_out;
+    int64_t lo, hi;
+    int64_t bad_requests;
+} sim_job;
+
+static void simulate_segment(sim_job *J, int64_t k)
+{
+    const orc_problem *P = J->P;
+    const int n = P->n, X = P->X, NC = P->n_classes;
+    const int64_t seg = J->seg_id[k];
+    const int64_t m = J->seg_m[k], rb = J->req_begin[k];
+    const uint64_t g0 = J->g0[k];
+    const double kp = P->k0[seg] * P->pue;
+    const double *q = prof(P, P->q, seg);
+
+    double *xs = (double *)malloc(sizeof(double) * (size_t)X * n);
+    int *ok = (int *)malloc(sizeof(int) * (size_t)X);
+    for (int j = 0; j < X; ++j) {
+        double obj, qlb; int vid, ml; uint64_t Tl[ORC_MAX_LEVELS];
+        ok[j] = solve_cell(P, seg, j, xs + (size_t)j * n, &obj, &qlb, &vid, Tl, &ml) == 0;
+    }
+    uint64_t *cnt = J->cnt + (size_t)k * X * NC * n;
+    uint64_t *tok = J->tok + (size_t)k * X * NC * n;
+    double *E = J->energy + (size_t)k * X, *Tm = J->time_s + (size_t)k * X;
+    double *Cb = J->carbon + (size_t)k * X, *Q = J->quality + (size_t)k * X;
+    uint64_t *sc = J->seg_count + (size_t)k * NC, *sp = J->seg_pinned + (size_t)k * NC;
+    uint64_t *st = J->seg_tok + (size_t)k * NC * n;
+    double *base = J->seg_base + (size_t)k * 4;
+    memset(cnt, 0, sizeof(uint64_t) * (size_t)X * NC * n);
+    memset(tok, 0, sizeof(uint64_t) * (size_t)X * NC * n);
+    for (int j = 0; j < X; ++j) { E[j] = 0.0; Tm[j] = 0.0; Cb[j] = 0.0; Q[j] = 0.0; }
+    memset(sc, 0, sizeof(uint64_t) * NC);
+    memset(sp, 0, sizeof(uint64_t) * NC);
+    memset(st, 0, sizeof(uint64_t) * NC * n);
+    base[0] = base[1] = base[2] = base[3] = 0.0;
+
+    for (int64_t r = 0; r < m; ++r) {
+        const int64_t ri = rb + r;
+        const uint64_t g = g0 + (uint64_t)r;
+        const uint32_t w = orc_draw_word(J->seed, g);
+        int pinned = 0, cls = 0;
+        if (J->flags) {
+            uint8_t f = J->flags[ri];
+            pinned = f & 1;
+            cls = (f >> 1) & 3;
+        }
+        if (cls >= NC) {                                /* invalid class: skipped */
+            J->bad_requests++;
+            if (J->levels_out)
+                for (int j = 0; j < X; ++j) J->levels_out[(size_t)j * J->pitch + ri] = 0xFF;
+            continue;
+        }
+        uint32_t t[ORC_MAX_LEVELS];
+        for (int i = 0; i < n; ++i) t[i] = J->tokens[(size_t)i * J->pitch + ri];
+
+        /* Base: every request at L0 */
+        {
+            double e0 = J->ef[cls * 8 + 0] + J->et[cls * 8 + 0] * (double)t[0];
+            double p0 = J->pf[cls * 8 + 0] + J->pt[cls * 8 + 0] * (double)t[0];
+            base[0] += e0;
+            base[1] += p0;
+            base[2] += orc_request_carbon(kp, P->k1, e0, p0);
+            base[3] += q[0];
+        }
+        sc[cls] += 1;
+        sp[cls] += (uint64_t)pinned;
+        for (int i = 0; i < n; ++i) st[cls * n + i] += t[i];
+
+        for (int j = 0; j < X; ++j) {
+            if (!ok[j]) {
+                if (J->levels_out) J->levels_out[(size_t)j * J->pitch + ri] = 0xFF;
+                continue;
+            }
+            int L = orc_select_level(n, xs + (size_t)j * n, w, pinned);
+            double el = J->ef[cls * 8 + L] + J->et[cls * 8 + L] * (double)t[L];
+            double pl = J->pf[cls * 8 + L] + J->pt[cls * 8 + L] * (double)t[L];
+            E[j] += el;
+            Tm[j] += pl;
+            Cb[j] += orc_request_carbon(kp, P->k1, el, pl);
+            Q[j] += q[L];
+            cnt[((size_t)j * NC + cls) * n + L] += 1;
+            tok[((size_t)j * NC + cls) * n + L] += t[L];
+            if (J->levels_out) J->levels_out[(size_t)j * J->pitch + ri] = (uint8_t)L;
+        }
+    }
+    free(xs);
+    free(ok);
+}
+
+static void *sim_worker(void *arg)
+{
+    sim_job *J = (sim_job *)arg;
+    for (int64_t k = J->lo; k < J->hi; ++k) simulate_segment(J, k);
+    return NULL;
+}
+
+/* Returns 0 ok, 1 invalid argument.  *bad_requests = requests skipped because
+ * their class index (flags bits 1-2) is >= n_classes.                       */
+int orc_simulate(int n, int R, int64_t T, int X,
+                 const double *k0, const double *kmin, const double *kmax, const double *xi,
+                 const double *e, const double *p, const double *q, int profile_per_interval,
+                 double k1, double pue,
+                 uint64_t seed, int n_classes, const double *ef, const double *et,
+                 const double *pf, const double *pt,
+                 int64_t n_sel, const int64_t *seg_id, const int64_t *req_begin,
+                 const int64_t *seg_m, const uint64_t *g0,
+                 const uint16_t *tokens, int64_t pitch, const uint8_t *flags,
+                 uint64_t *cnt, uint64_t *tok, double *energy, double *time_s,
+                 double *carbon, double *quality,
+                 uint64_t *seg_count, uint64_t *seg_pinned, uint64_t *seg_tok, double *seg_base,
+                 uint8_t *levels_out, int n_threads, int64_t *bad_requests)
+{
+    if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1) return 1;
+    if (n_classes < 1 || n_classes > ORC_MAX_CLASSES) return 1;
+    if (!(pue >= 1.0 && pue <= DBL_MAX) || !(k1 >= 0.0 && k1 <= DBL_MAX)) return 1;
+    for (int64_t k = 0; k < n_sel; ++k)
+        if (seg_id[k] < 0 || seg_id[k] >= (int64_t)R * T || seg_m[k] < 0) return 1;
+    orc_problem P = { n, R, X, profile_per_interval, n_classes, T, k0, kmin, kmax, xi, e, p, q, k1, pue };
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > 256) n_threads = 256;
+    if (n_sel < n_threads) n_threads = n_sel > 0 ? (int)n_sel : 1;
+
+    sim_job jobs[256];
+    pthread_t th[256];
+    for (int t = 0; t < n_threads; ++t) {
+        sim_job J = { &P, seed, ef, et, pf, pt, seg_id, req_begin, seg_m, g0, tokens, pitch, flags,
+                      cnt, tok, energy, time_s, carbon, quality, seg_count, seg_pinned, seg_tok,
+                      seg_base, levels_out, n_sel * t / n_threads, n_sel * (t + 1) / n_threads, 0 };
+        jobs[t] = J;
+    }
+    if (n_threads == 1) {
+        sim_worker(&jobs[0]);
+    } else {
+        for (int t = 0; t < n_threads; ++t) pthread_create(&th[t], NULL, sim_worker, &jobs[t]);
+        for (int t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
+    }
+    int64_t bad = 0;
+    for (int t = 0; t < n_threads; ++t) bad += jobs[t].bad_requests;
+    if (bad_requests) *bad_requests = bad;
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Group totals (conservation S:485): per (region, xi) and per
+ * xi, summed sequentially over cells in (region, interval) order.  Stats
+ * k = 0..K-1 with K = 11 + 2n:
+ *   0 requests, 1 pinned, 2 energy kWh, 3 time s, 4 carbon g, 5 quality
+ *   (sum q[level]), 6..9 Base energy/time/carbon/quality (all-L0),
+ *   10 expected carbon (m * LP objective, Eq. 2), 11..11+n-1 requests per
+ *   level, 11+n..11+2n-1 generated tokens per level.
+ * Inputs are this oracle's own per-cell / per-segment results for ALL
+ * segments [first_segment, first_segment + n_segments).  Output layout:
+ * group[R][X][K] followed by global[X][K]; rows of regions outside the
+ * segment range are zero.                                                   */
+int orc_reduce(int n, int R, int64_t T, int X, int n_classes,
+               int64_t first_segment, int64_t n_segments,
+               const uint8_t *cell_status, const double *objective,
+               const uint64_t *cnt, const uint64_t *tok, const double *energy,
+               const double *time_s, const double *carbon, const double *quality,
+               const uint64_t *seg_count, const uint64_t *seg_pinned, const double *seg_base,
+               double *out)
+{
+    const int K = 11 + 2 * n;
+    const int NC = n_classes;
+    memset(out, 0, sizeof(double) * (size_t)(R + 1) * X * K);
+    for (int64_t s = 0; s < n_segments; ++s) {
+        int64_t r = (first_segment + s) / T;
+        double m = 0.0, pin = 0.0;
+        for (int c = 0; c < NC; ++c) { m += (double)seg_count[s * NC + c]; pin += (double)seg_pinned[s * NC + c]; }
+        for (int j = 0; j < X; ++j) {
+            int64_t cell = s * X + j;
+            double *G = out + ((size_t)r * X + j) * K;
+            G[0] += m;
+            G[1] += pin;
+            G[6] += seg_base[s * 4 + 0];
+            G[7] += seg_base[s * 4 + 1];
+            G[8] += seg_base[s * 4 + 2];
+            G[9] += seg_base[s * 4 + 3];
+            if (cell_status[cell] != 0) continue;
+            G[2] += energy[cell];
+            G[3] += time_s[cell];
+            G[4] += carbon[cell];
+            G[5] += quality[cell];
+            G[10] += m * objective[cell];
+            for (int L = 0; L < n; ++L) {
+                double cL = 0.0, tL = 0.0;
+                for (int c = 0; c < NC; ++c) {
+                    cL += (double)cnt[(cell * NC + c) * n + L];
+                    tL += (double)tok[(cell * NC + c) * n + L];
+                }
+                G[11 + L] += cL;
+                G[11 + n + L] += tL;
+            }
+        }
+    }
+    double *glob = out + (size_t)R * X * K;
+    for (int r = 0; r < R; ++r)
+        for (int j = 0; j < X; ++j)
+            for (int k = 0; k < K; ++k)
+                glob[(size_t)j * K + k] += out[((size_t)r * X + j) * K + k];
+    return 0;
+}
