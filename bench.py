@@ -1,0 +1,435 @@
+#!/usr/bin/env python3
+"""Benchmark of the Sprout hot path (solve -> simulate -> reduce [-> NCCL
+allreduce]) on synthetic BASELINE.json workloads.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl sprout|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line (rank 0).  A "step" is one pass of the whole hot path
+over the workload: every LP cell solved, every request of the trace streamed
+and assigned in every xi cell of its segment, group totals reduced (and
+all-reduced across ranks).  Inputs are resident in HBM before timing
+(`value`); `e2e` re-measures the same metric through the host-buffer C-ABI
+call (sprout_sweep_host) with the H2D copy of the trace and the D2H of the
+totals inside the timed region.  `--impl reference` times the CPU oracle
+(the only reference this paper-only tier has) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "requests simulated/s and LP cells/s at 1/2/4/8 B200; % of HBM peak"
+UNIT = "requests/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def workload_desc(w):
+    P = w.prob
+    return (f"{w.name}: {P.R} regions x {P.T} CI intervals x {P.X} xi x {P.n} directive levels, "
+            f"{w.N:,} requests, {w.cost.n_classes} model class(es), flags={'yes' if w.spec.has_flags else 'no'}")
+
+
+def algorithmic_bytes(w, sh):
+    """Bytes the method must move in one sprout_simulate_trace launch
+    (DESIGN.md 'Roofline'): the token planes (+flags) once, the segment
+    offsets, k0, every cell's thresholds/max_level/status, and the per-cell
+    and per-segment outputs."""
+    P = w.prob
+    n, X, NC = P.n, P.X, w.cost.n_classes
+    S = sh.n_segments
+    C = S * X
+    N = int(sh.seg_offsets[-1] - sh.seg_offsets[0])
+    f = 1 if w.spec.has_flags else 0
+    b = N * (2 * n + f)                              # trace
+    b += 8 * (S + 1) + 8 * S                         # seg_offsets, k0
+    b += C * (4 * (n - 1) + 1 + 1)                   # thresholds, max_level, cell_status
+    b += C * (NC * n * 16 + 32)                      # cnt, tok, energy/time/carbon/quality
+    b += S * (NC * (2 + n) * 8 + 32)                 # segment stats + Base
+    return b
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU oracle
+
+
+def oracle_sample_run(w, seg_ids, threads):
+    """Oracle on a set of whole segments of the workload (LP + replay),
+    tokens regenerated on the host (generation not timed)."""
+    import oracle
+    parts, begins, ms, g0s = [], [], [], []
+    pos = 0
+    off = w.spec.seg_offsets
+    flags_parts = []
+    for s in seg_ids:
+        a, b = int(off[s]), int(off[s + 1])
+        t, f = synth.gen_tokens(w.spec, a, b)
+        parts.append(t); flags_parts.append(f)
+        begins.append(pos); ms.append(b - a); g0s.append(a); pos += b - a
+    toks = np.concatenate(parts, axis=1) if parts else np.zeros((w.prob.n, 0), np.uint16)
+    flags = np.concatenate(flags_parts) if w.spec.has_flags and parts else None
+    t0 = time.perf_counter()
+    oracle.simulate(w.prob, w.cost, np.asarray(seg_ids), np.array(begins), np.array(ms),
+                    np.array(g0s, np.uint64), toks, flags, threads=threads)
+    dt = time.perf_counter() - t0
+    return pos, len(seg_ids), dt
+
+
+def oracle_baseline(w, target_s=12.0):
+    """cpu_baseline: the oracle as it stands on the host cores, on a bounded,
+    deterministic segment sample of the same workload (calibrated to
+    ~target_s of CPU time)."""
+    import oracle
+    oracle.build()
+    threads = os.cpu_count() or 1
+    S = w.prob.R * w.prob.T
+    off = w.spec.seg_offsets
+    m = np.diff(off)
+    # calibration on a few segments
+    ids = synth.sample_segments(w.spec, 0, S, every=max(1, S // max(threads, 8)))[: max(threads, 8)]
+    req, _, dt = oracle_sample_run(w, ids, threads)
+    rate = req / max(dt, 1e-6)
+    want = int(rate * target_s)
+    every = max(1, int(np.ceil(w.N / max(want, 1))))
+    ids = synth.sample_segments(w.spec, 0, S, every=every)
+    req, nseg, dt = oracle_sample_run(w, ids, threads)
+    return {"value": req / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{nseg} whole segments (every {every}th + first/last/largest) = {req:,} requests x "
+                      f"{w.prob.X} xi cells, LP solves included, token generation excluded; {dt:.2f} s",
+            "lp_cells_per_s": nseg * w.prob.X / dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = synth.make_workload(args.config)
+    import oracle
+    oracle.build()
+    threads = os.cpu_count() or 1
+    S = w.prob.R * w.prob.T
+    # each step: a bounded sample sized to ~2 s of host time
+    ids = synth.sample_segments(w.spec, 0, S, every=max(1, S // 64))[:64]
+    req, _, dt = oracle_sample_run(w, ids, threads)
+    rate = req / max(dt, 1e-6)
+    every = max(1, int(np.ceil(w.N / max(int(rate * 2.0), 1))))
+    ids = synth.sample_segments(w.spec, 0, S, every=every)
+    for _ in range(args.warmup):
+        oracle_sample_run(w, ids, threads)
+    times, reqs = [], 0
+    for _ in range(args.steps):
+        r, nseg, dt = oracle_sample_run(w, ids, threads)
+        times.append(dt); reqs += r
+    total = sum(times)
+    value = reqs / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/u32",
+            "data": "synthetic", "config": {"workload": workload_desc(w), "sample_segments": int(len(ids))},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                             "sample": f"{len(ids)} whole segments per step (every {every}th + first/last/largest), "
+                                       f"{reqs // max(args.steps, 1):,} requests per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------- GPU arm
+
+
+def run_sprout(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2403_12900_b200 import sprout as S
+    from paper_2403_12900_b200.runner import Sweep
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    w = synth.make_workload(args.config)
+    sh = synth.shard(w.spec, world, rank)
+    sw = Sweep(w.prob, w.cost, sh, dev, spec=w.spec)
+    stream = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    trace_bytes = sw.trace.tokens.numel() * 2 + (sw.trace.flags.numel() if sw.trace.flags is not None else 0)
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = trace_bytes < 4 * l2 or args.flush_l2
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+
+    launches = [0]
+
+    def step(ev=None):
+        sw.solve(); launches[0] += S.last_launch_count()
+        if ev is not None:
+            ev[0].record(stream)
+        sw.simulate(); launches[0] += S.last_launch_count()
+        if ev is not None:
+            ev[1].record(stream)
+        sw.reduce(); launches[0] += S.last_launch_count()
+        if world > 1:
+            dist.all_reduce(sw.group)
+
+    for _ in range(args.warmup):
+        if flush:
+            flush_buf.zero_()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches[0] = 0
+    sim_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for k in range(args.steps):
+            if flush:
+                flush_buf.zero_()       # L2 flush between steps (outside the per-step events)
+            step_ev[k][0].record(stream)
+            step(sim_ev[k])
+            step_ev[k][1].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    sim_ms = [a.elapsed_time(b) for a, b in sim_ev]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+
+    # LP cells/s: the solve kernel alone
+    lp_ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    lp_ev[0].record(stream)
+    for _ in range(args.steps):
+        sw.solve()
+    lp_ev[1].record(stream)
+    torch.cuda.synchronize()
+    lp_ms = lp_ev[0].elapsed_time(lp_ev[1]) / args.steps
+    lp_t = torch.tensor([lp_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(lp_t, op=dist.ReduceOp.MAX)
+    lp_ms = float(lp_t.item())
+
+    status = int(sw.totals.trace_status.item())
+    g = sw.group.cpu().numpy()
+
+    # e2e: the host-buffer C-ABI call (H2D of the trace + D2H of the totals timed)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, w, sh, sw, dev, world)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    alg = algorithmic_bytes(w, sh)
+    sim_avg_ms = statistics.mean(sim_ms)
+    achieved = alg / (sim_avg_ms * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        d = json.load(open(tf))
+        if d.get("workload") == w.name and d.get("n_gpus", 1) == world:
+            traffic = d.get("dram_bytes_per_launch")
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = oracle_baseline(w, args.cpu_seconds)
+    N = w.N
+    line = {
+        "metric": METRIC, "value": N / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64/u32", "data": "synthetic",
+        "config": {"workload": workload_desc(w), "config": w.name, "requests": N, "lp_cells": w.prob.C,
+                   "parallelism": f"segments sharded over {world} GPU(s), one NCCL allreduce of group totals",
+                   "l2": ("flushed (256 MB memset) between steps" if flush else
+                          f"inputs larger than L2 (trace {trace_bytes / 1e9:.2f} GB/GPU > L2 {l2 / 1e6:.0f} MB)")},
+        "lp_cells_per_s": w.prob.C / (lp_ms * 1e-3),
+        "request_cells_per_s": N * w.prob.X / (ms_per_step * 1e-3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "sprout_simulate_trace (prep + trace_kernel, CUDA events)",
+                     "algorithmic_bytes_per_launch": alg, "launch_ms": sim_avg_ms, "peak_source": peak_src},
+        "clocks": clk.summary(),
+        "gpu_launches": launches[0],
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "trace_status": status,
+        "check": {"requests_counted": float(g[-1, 0, 0]),
+                  "carbon_saving_xi_max": float(1 - g[-1, -1, 4] / g[-1, -1, 8]) if g[-1, -1, 8] > 0 else None},
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(args, w, sh, sw, dev, world):
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from paper_2403_12900_b200 import sprout as S
+
+    P = w.prob
+    tok_dev = sw.trace.tokens
+    tok_host = torch.empty(tok_dev.shape, dtype=tok_dev.dtype, pin_memory=True)
+    tok_host.copy_(tok_dev)
+    fl_host = None
+    if sw.trace.flags is not None:
+        fl_host = torch.empty(sw.trace.flags.shape, dtype=torch.uint8, pin_memory=True)
+        fl_host.copy_(sw.trace.flags)
+    keep = []
+
+    def pinned(a, dt):
+        t = torch.from_numpy(np.ascontiguousarray(a, dt)).pin_memory()
+        keep.append(t)
+        return t.data_ptr()
+
+    lp = S.LpProblem(P.n, P.R, P.T, P.X, P.profile_per_interval, pinned(P.k0, np.float64),
+                     pinned(P.kmin, np.float64), pinned(P.kmax, np.float64), pinned(P.xi, np.float64),
+                     pinned(P.e, np.float64), pinned(P.p, np.float64), pinned(P.q, np.float64), P.k1, P.pue,
+                     sh.first_segment, sh.n_segments)
+    tr = S.Trace(sh.n_requests, sh.first_request, pinned(sh.seg_offsets, np.int64), tok_host.data_ptr(),
+                 tok_dev.shape[1], fl_host.data_ptr() if fl_host is not None else None)
+    cm = S.cost_model(w.cost)
+    ws = S.workspace(S.sweep_workspace_bytes(lp, tr, w.cost.n_classes), dev)
+    out = torch.zeros((P.R + 1) * P.X * S.group_stat_count(P.n), dtype=torch.float64).pin_memory().numpy()
+    st = torch.zeros(1, dtype=torch.int32).pin_memory().numpy()
+    stream = torch.cuda.current_stream()
+    steps = max(3, min(args.steps, args.e2e_steps))
+    for _ in range(2):
+        S.sweep_host(lp, tr, cm, out, st, ws)
+    if world > 1:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        S.sweep_host(lp, tr, cm, out, st, ws)
+        if world > 1:
+            g = torch.from_numpy(out).to(dev)
+            dist.all_reduce(g)
+            out[:] = g.cpu().numpy()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    h2d = (tok_host.numel() * 2 + (fl_host.numel() if fl_host is not None else 0) + (sh.n_segments + 1) * 8
+           + P.k0.size * 8 + (P.e.size + P.p.size + P.q.size + P.xi.size + 2 * P.R) * 8)
+    d2h = out.size * 8 + 4
+    del ws
+    return {"value": w.N / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": ms, "steps": steps, "api": "sprout_sweep_host (C ABI, pinned host buffers)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C4", choices=synth.CONFIGS)
+    ap.add_argument("--impl", default="sprout", choices=["sprout", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--flush-l2", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_sprout(args)
+
+
+if __name__ == "__main__":
+    main()

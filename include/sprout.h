@@ -1,0 +1,247 @@
+/*
+ * sprout.h -- C ABI of the B200-native Sprout hot path (arXiv 2403.12900).
+ *
+ * The path, per (region r x carbon-intensity interval t x quality
+ * coefficient xi_j) cell:
+ *   1. sprout_solve_directives: quality floor q_lb (Eq. 3), the
+ *      expected-carbon cost vector c (Eq. 2, with PUE) and
+ *      the directive LP  min c.x  s.t. q.x >= q_lb, 0 <= x <= 1, sum x = 1
+ *      (Eqs. 4-7), solved exactly by vertex enumeration in fp64;
+ *      plus the inverse-CDF thresholds of the solved mix x.
+ *   2. sprout_simulate_trace: for every request of the cell's interval, a
+ *      counter-based Philox4x32-10 draw selects a directive level from x
+ *      (selector (1); opted-out users always L0); its energy,
+ *      time and carbon follow Eq. 1 with E, T linear in the
+ *      generated tokens; per-cell totals are reduced.
+ *   3. sprout_reduce_totals: per (region, xi) and per xi group totals; the
+ *      caller then all-reduces them across GPUs (NCCL, torch.distributed).
+ * P:<line> cites /root/reference/PAPER.md.  Readings of silent or ambiguous
+ * passages (tie-break, rounding order, RNG layout, ...) are DESIGN.md L1-L16.
+ *
+ * Conventions
+ *   - Every array pointer inside the structs is a DEVICE pointer (cudaMalloc
+ *     / torch CUDA tensor) owned by the caller, except where a function says
+ *     HOST.  The library allocates nothing persistent and keeps no global
+ *     state: calls are thread-safe and asynchronous on `stream`.
+ *   - Host-checkable arguments are validated synchronously before anything
+ *     is enqueued; a non-OK status means nothing was launched.
+ *   - Data in device arrays is validated on the device, per cell
+ *     (cell_status) or per trace (trace_status), without a host sync.
+ *   - Cells are indexed cell = (s - first_segment) * n_xi + j with segment
+ *     s = r * n_intervals + t (xi innermost).
+ */
+#ifndef SPROUT_H
+#define SPROUT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+struct CUstream_st;                       /* the CUDA runtime's cudaStream_t */
+typedef struct CUstream_st *sprout_stream;
+
+typedef enum {
+    SPROUT_OK = 0,
+    SPROUT_ERR_INVALID_ARGUMENT = 1,  /* bad scalar, NULL required pointer, misalignment, range */
+    SPROUT_ERR_INFEASIBLE = 2,        /* sprout_check_cells: some cell infeasible (status 2) */
+    SPROUT_ERR_OVERFLOW = 3,          /* sizes whose counts could exceed 2^53 / index ranges */
+    SPROUT_ERR_CUDA = 4,              /* a CUDA runtime call or launch failed (incl. no device) */
+    SPROUT_ERR_INVALID_CELL = 5       /* sprout_check_cells: some cell had invalid inputs (status 1) */
+} sprout_status;
+
+#define SPROUT_MAX_LEVELS 8
+#define SPROUT_MAX_CLASSES 4
+#define SPROUT_MAX_XI 4096
+
+/* cell_status codes (device, one byte per cell) */
+#define SPROUT_CELL_OK 0
+#define SPROUT_CELL_INVALID 1     /* xi not in [0,1]; q_i not in [0,1]; NaN/inf; negative k0/e/p; kmax < kmin */
+#define SPROUT_CELL_INFEASIBLE 2  /* no feasible vertex (impossible when q_lb <= q0) */
+
+/* trace_status bits (device word, OR-ed) */
+#define SPROUT_TRACE_BAD_CLASS   0x1u   /* a request's class (flags bits 1-2) >= n_classes: request skipped */
+#define SPROUT_TRACE_BAD_OFFSETS 0x2u   /* seg_offsets not non-decreasing within [0, n_requests]: segment skipped */
+#define SPROUT_TRACE_SLOW_PATH   0x100u /* informational: a segment needed the generic (slow) kernel path */
+
+/* ---------------------------------------------------------------------- */
+/* The directive LP over a (region x interval x xi) grid, Eqs. 2-7.        */
+typedef struct {
+    int32_t n_levels;          /* n: directive levels L0..L(n-1), L0 = no directive; 1..8 */
+    int32_t n_regions;         /* R >= 1 */
+    int64_t n_intervals;       /* T >= 1 carbon-intensity intervals per region (zero-order hold) */
+    int32_t n_xi;              /* X: 1..SPROUT_MAX_XI quality coefficients */
+    int32_t profile_per_interval; /* 0: e,p,q are [R][n]; 1: they are [R*T][n] */
+    const double *k0;          /* [R*T] carbon intensity, gCO2/kWh */
+    const double *k0_min;      /* [R] historical minimum (Table II) */
+    const double *k0_max;      /* [R] historical maximum */
+    const double *xi;          /* [X] paper xi in [0,1]: allowed quality deviation */
+    const double *e;           /* [R|R*T][n] mean energy per request at each level, kWh */
+    const double *p;           /* [R|R*T][n] mean processing time per request, s */
+    const double *q;           /* [R|R*T][n] preference rate of each level, in [0,1] */
+    double k1;                 /* embodied carbon rate CO2_embed / T_life, gCO2/s; >= 0 */
+    double pue;                /* power usage effectiveness, >= 1 (reading L2) */
+    int64_t first_segment;     /* this call covers segments [first_segment, first_segment + n_segments) */
+    int64_t n_segments;        /* of the R*T grid (a rank's shard) */
+} sprout_lp_problem;
+
+/* Outputs of sprout_solve_directives, one entry per local cell. */
+typedef struct {
+    double *x;                 /* [cells][n] the solved mix: probability of each level */
+    double *objective;         /* [cells] expected gCO2 per request f(x) (Eq. 2) */
+    double *q_lb;              /* [cells] the quality floor b of Eq. 3 */
+    uint8_t *vertex;           /* [cells] optimal vertex: i = pure level i; n + k = k-th pair (i<j)
+                                  in lexicographic order; 255 = none (invalid/infeasible) */
+    uint32_t *threshold;       /* [cells][n-1] inverse-CDF thresholds T_i = min(ceil(cum_i 2^32), 2^32),
+                                  2^32 stored saturated as 0xFFFFFFFF; may be NULL iff n == 1 */
+    uint8_t *max_level;        /* [cells] first i with T_i = 2^32, else n-1 */
+    uint8_t *cell_status;      /* [cells] SPROUT_CELL_* */
+} sprout_lp_solution;
+
+/* A rank's slice of the request trace. */
+typedef struct {
+    int64_t n_requests;        /* local requests held in the buffers */
+    uint64_t first_request;    /* global index of local request 0 (Philox counter base); multiple of 8 */
+    const int64_t *seg_offsets;/* [n_segments+1] local request offsets of the segments (CSR) */
+    const uint16_t *tokens;    /* [n][plane_pitch] generated tokens of each request at each level */
+    int64_t plane_pitch;       /* elements; multiple of 8, >= n_requests; tokens 16-byte aligned */
+    const uint8_t *flags;      /* [plane_pitch] or NULL: bit0 = opted-out user (always L0),
+                                  bits1-2 = model class (cost-model row); 16-byte aligned */
+} sprout_trace;
+
+/* Per-request energy/time model and the selection seed (HOST struct, by pointer).
+ * E = ef[c][L] + et[c][L]*tok, T = pf[c][L] + pt[c][L]*tok (reading L11). */
+typedef struct {
+    uint64_t seed;             /* Philox key (lo32, hi32) of the selection draws (reading L10) */
+    int32_t n_classes;         /* 1..4 */
+    int32_t reserved;
+    double ef[SPROUT_MAX_CLASSES][SPROUT_MAX_LEVELS];  /* kWh */
+    double et[SPROUT_MAX_CLASSES][SPROUT_MAX_LEVELS];  /* kWh per generated token */
+    double pf[SPROUT_MAX_CLASSES][SPROUT_MAX_LEVELS];  /* s */
+    double pt[SPROUT_MAX_CLASSES][SPROUT_MAX_LEVELS];  /* s per generated token */
+} sprout_cost_model;
+
+/* Outputs of sprout_simulate_trace (all written in full; no pre-zeroing needed). */
+typedef struct {
+    uint64_t *cnt;             /* [cells][n_classes][n] requests assigned each level */
+    uint64_t *tok;             /* [cells][n_classes][n] generated tokens at the assigned level */
+    double *energy_kwh;        /* [cells] sum of E over the cell's requests */
+    double *time_s;            /* [cells] sum of T */
+    double *carbon_g;          /* [cells] sum of Eq. 1 carbon (k0*PUE*E + k1*T) */
+    double *quality;           /* [cells] sum of q[level] (reading L15) */
+    uint64_t *seg_count;       /* [n_segments][n_classes] requests per segment */
+    uint64_t *seg_pinned;      /* [n_segments][n_classes] opted-out requests */
+    uint64_t *seg_tok;         /* [n_segments][n_classes][n] sum of tokens at every level (all requests) */
+    double *seg_base;          /* [n_segments][4] Base counterfactual (all at L0):
+                                  energy, time, carbon, quality */
+    uint32_t *trace_status;    /* [1] SPROUT_TRACE_* bits */
+} sprout_cell_totals;
+
+/* Harness-only synthetic trace generator (not part of the method). */
+typedef struct {
+    uint64_t gen_seed;         /* Philox key of the generator (stream 1) */
+    uint64_t first_request;    /* global index of local request 0 */
+    int64_t n_requests;
+    int32_t n_levels;          /* 1..8 */
+    int32_t n_classes;         /* 1..4 */
+    uint32_t pin_thresh;       /* pinned iff (w3 & 0xFFFFFF) < pin_thresh */
+    uint32_t reserved;
+    const uint16_t *q0_table;  /* [n_classes][4096] L0 generated-token quantiles */
+    const uint16_t *ratio_table; /* [8][256] per-level length ratios, fixed point 2^-16 */
+} sprout_trace_generator;
+
+/* ---------------------------------------------------------------------- */
+
+/* Step 1 (a1-a4).  One thread per cell: Eq. 3 floor, Eq. 2 cost vector,
+ * vertex enumeration in a fixed order keeping the first strict minimum
+ * (pure levels ascending, then pairs lexicographically; reading L6), IEEE
+ * fp64 without contraction (reading L7), thresholds.  Writes every field of
+ * `solution` for the n_segments*n_xi local cells.  Errors: INVALID_ARGUMENT
+ * (n outside [1,8], R/T/X < 1 or X > SPROUT_MAX_XI, shard outside R*T, PUE < 1
+ * or NaN, k1 < 0 or NaN, NULL pointers); CUDA on launch failure. */
+sprout_status sprout_solve_directives(const sprout_lp_problem *problem,
+                                      const sprout_lp_solution *solution,
+                                      sprout_stream stream);
+
+/* Bytes of device workspace sprout_simulate_trace needs (0 on invalid args). */
+size_t sprout_workspace_bytes(const sprout_lp_problem *problem, const sprout_trace *trace);
+
+/* Step 2 (a5-a8).  Streams the trace once.  Selection draw of global
+ * request g: Philox4x32-10, key = (seed lo32, seed hi32), counter =
+ * (g>>2 lo32, g>>2 hi32, 0, 0), word g&3 (reading L10); one draw per request
+ * shared by all xi cells of its segment.  level = pinned ? 0 :
+ * min(#{i <= n-2 : w >= T_i}, max_level).  Cells with cell_status != 0 are
+ * skipped (totals 0).  `levels_out` (verify mode, slow) is NULL or
+ * [n_xi][plane_pitch]: level of every request for every cell of its
+ * segment (0xFF for skipped cells).  Errors: INVALID_ARGUMENT (as above, plus
+ * NULL tokens/seg_offsets/outputs, misaligned tokens/flags, pitch, first_request
+ * not a multiple of 8, n_classes outside [1,4], workspace too small); OVERFLOW
+ * (n_requests >= 2^40); CUDA. */
+sprout_status sprout_simulate_trace(const sprout_lp_problem *problem,
+                                    const sprout_lp_solution *solution,
+                                    const sprout_trace *trace,
+                                    const sprout_cost_model *cost,
+                                    const sprout_cell_totals *totals,
+                                    uint8_t *levels_out,
+                                    void *workspace, size_t workspace_bytes,
+                                    sprout_stream stream);
+
+/* Number of statistics K per group row: 11 + 2n.  Row layout: 0 requests,
+ * 1 opted-out, 2 energy kWh, 3 time s, 4 carbon g, 5 quality, 6-9 Base
+ * energy/time/carbon/quality, 10 expected carbon (requests x objective),
+ * 11.. requests per level (n), 11+n.. tokens per level (n). */
+int32_t sprout_group_stat_count(int32_t n_levels);
+
+/* Bytes of device workspace sprout_reduce_totals needs. */
+size_t sprout_reduce_workspace_bytes(const sprout_lp_problem *problem);
+
+/* Step 3 (a9, local part).  group_totals (device, fp64) = [R][X][K] followed
+ * by [X][K]; rows of regions outside the shard are 0.  Integer statistics
+ * are exact in fp64 (< 2^53).  The caller all-reduces group_totals (SUM)
+ * across ranks.  Deterministic (fixed summation order). */
+sprout_status sprout_reduce_totals(const sprout_lp_problem *problem,
+                                   const sprout_lp_solution *solution,
+                                   const sprout_cell_totals *totals,
+                                   int32_t n_classes,
+                                   double *group_totals,
+                                   void *workspace, size_t workspace_bytes,
+                                   sprout_stream stream);
+
+/* Blocking helper: worst cell_status over the local cells -> OK,
+ * INVALID_CELL or INFEASIBLE.  Synchronises `stream`. */
+sprout_status sprout_check_cells(const sprout_lp_problem *problem,
+                                 const sprout_lp_solution *solution,
+                                 sprout_stream stream);
+
+/* End-to-end call with HOST buffers: copies the problem arrays and the trace
+ * from host memory (pinned for full speed) into `device_workspace`, runs
+ * steps 1-3 and copies the [R+1][X][K] group totals back into
+ * `host_group_totals`; synchronises `stream` before returning.  Every array
+ * pointer inside `problem` and `trace` is a HOST pointer here. */
+size_t sprout_sweep_workspace_bytes(const sprout_lp_problem *problem, const sprout_trace *trace,
+                                    int32_t n_classes);
+sprout_status sprout_sweep_host(const sprout_lp_problem *problem, const sprout_trace *trace,
+                                const sprout_cost_model *cost, double *host_group_totals,
+                                uint32_t *host_trace_status,
+                                void *device_workspace, size_t device_workspace_bytes,
+                                sprout_stream stream);
+
+/* Harness only: synthetic Llama2-shaped trace (not part of the method).
+ * Writes tokens [n][plane_pitch] and (if flags != NULL) flags [plane_pitch]
+ * for local requests [0, n_requests). */
+sprout_status sprout_generate_trace(const sprout_trace_generator *gen,
+                                    uint16_t *tokens, int64_t plane_pitch, uint8_t *flags,
+                                    sprout_stream stream);
+
+/* Number of kernel launches (not memsets) the last successful call of each
+ * entry point on this thread enqueued -- for launch accounting in benches. */
+int32_t sprout_last_launch_count(void);
+
+const char *sprout_status_string(sprout_status status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPROUT_H */

@@ -1,0 +1,105 @@
+// sprout_kernels.cuh -- kernel argument blocks and launchers (host <-> device).
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+#include "sprout_device.cuh"
+
+namespace sprout {
+
+struct LpArgs {
+    int n, X;
+    int64_t T, first_segment, n_segments;
+    int profile_per_interval;
+    const double *k0, *kmin, *kmax, *xi, *e, *p, *q;
+    double k1, pue;
+    double *x, *objective, *q_lb;
+    uint8_t *vertex;
+    uint32_t *threshold;
+    uint8_t *max_level, *cell_status;
+};
+
+// Simulation plan shared by the prep and the streaming kernels.
+struct SimPlan {
+    int n, X, NC;
+    int kcap;          // max distinct breakpoints per segment on the fast path; -1 = all slow
+    int nb;            // bins per class in the warp histograms: kcap+1 draw bins, a total slot, the pinned bin
+    int nw;            // 32-bit histogram words per entry = ceil((n+1)/2)
+    int kp;            // key slots per segment in shared memory (power of two >= kcap+1)
+    int warps_per_cta;
+    size_t warp_smem;  // bytes of shared memory per warp
+    int ctas;          // persistent grid size
+    int sort_cap;      // power of two >= X*(n-1) (prep sort buffer), 0 if none
+};
+
+struct SimArgs {
+    // problem / shard
+    int n, X, NC;
+    int64_t T, first_segment, n_segments;
+    int profile_per_interval;
+    const double *k0, *q;      // q rows for the quality sums
+    double k1, pue;
+    // solution
+    const uint32_t *threshold;
+    const uint8_t *max_level, *cell_status;
+    // trace
+    int64_t n_requests;
+    uint64_t first_request;
+    const int64_t *seg_offsets;
+    const uint16_t *tokens;
+    int64_t pitch;
+    const uint8_t *flags;
+    uint64_t seed;
+    // outputs
+    uint64_t *cnt, *tok;
+    double *energy, *time_s, *carbon, *quality;
+    uint64_t *seg_count, *seg_pinned, *seg_tok;
+    double *seg_base;
+    uint32_t *trace_status;
+    uint8_t *levels_out;
+    // workspace
+    uint32_t *queue;           // work counter
+    int32_t *seg_meta;         // [n_segments] K, -1 slow, -2 bad offsets
+    uint32_t *seg_keys;        // [n_segments][kcap] sorted distinct breakpoints minus one
+    uint16_t *seg_bnd;         // [n_segments][X][n-1] first bin of each level >= 1
+    // plan
+    int kcap, nb, nw, kp, sort_cap;
+    size_t warp_smem;
+    CostConst cost;
+};
+
+struct ReduceArgs {
+    int n, X, NC, R, K;
+    int64_t T, first_segment, n_segments;
+    int64_t r_lo, r_hi;        // regions touched by the shard
+    int chunk, n_chunks;       // intervals per stage-1 block
+    const uint8_t *cell_status;
+    const double *objective;
+    const uint64_t *cnt, *tok;
+    const double *energy, *time_s, *carbon, *quality;
+    const uint64_t *seg_count, *seg_pinned;
+    const double *seg_base;
+    double *partials;          // [r_hi-r_lo][n_chunks][X][K]
+    double *out;               // [R+1][X][K]
+};
+
+struct GenArgs {
+    uint64_t gen_seed, first_request;
+    int64_t n_requests, pitch;
+    int n, NC;
+    uint32_t pin_thresh;
+    const uint16_t *q0_table, *ratio_table;
+    uint16_t *tokens;
+    uint8_t *flags;
+};
+
+cudaError_t launch_lp_solve(const LpArgs &a, cudaStream_t stream, int *launches);
+bool make_sim_plan(int n, int X, int NC, SimPlan *plan);
+size_t sim_workspace_bytes(const SimPlan &plan, int64_t n_segments);
+cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStream_t stream, int *launches);
+size_t reduce_workspace_bytes(int n, int X, int R, int64_t T, int64_t first_segment, int64_t n_segments);
+cudaError_t launch_reduce(ReduceArgs &a, void *ws, cudaStream_t stream, int *launches);
+cudaError_t launch_generate(const GenArgs &a, cudaStream_t stream, int *launches);
+cudaError_t launch_check_cells(const uint8_t *status, int64_t n_cells, uint32_t *out, cudaStream_t stream, int *launches);
+
+}  // namespace sprout

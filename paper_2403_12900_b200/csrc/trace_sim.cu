@@ -1,0 +1,790 @@
+// trace_sim.cu -- step 2 of the hot path: stream the request trace once,
+// select a directive level for every request in every xi cell of its
+// segment, and reduce per-cell totals.
+//
+// Design:
+//  * All X cells of a segment share one Philox draw per request (reading
+//    L10).  A cell's level is a step function of the draw w with steps at its
+//    thresholds, so every cell of the segment is determined by which BIN of
+//    the segment's merged, sorted, distinct breakpoints w falls in.  The
+//    prep kernel builds that breakpoint list and, per cell, the first bin of
+//    each level.  The streaming kernel then only needs, per request, the bin
+//    (a branchless binary search over <= X+1 keys) and one add of
+//    (1, tok_0..tok_{n-1}) into a histogram; every cell's exact integer
+//    statistics are differences of histogram prefix sums (a8), and its fp64
+//    energy/time/carbon/quality follow from them in closed form (Eq. 1 is
+//    linear in (count, tokens)).
+//  * Histograms are lane-private in shared memory (no atomics on the hot
+//    path): 16-bit packed fields, two per 32-bit word, with a guard bit that
+//    spills a word into 64-bit warp accumulators before it can overflow.
+//  * One warp owns one segment at a time (dynamic queue), so segment totals
+//    need no cross-CTA reduction and are written with plain stores.
+//  * Token planes are read once with 128-bit streaming loads, prefetched
+//    two groups ahead.
+// Segments the fast path cannot represent (more than kcap distinct
+// breakpoints; arbitrary user thresholds) use a generic per-cell path.
+#include <cuda_runtime.h>
+#include "sprout_device.cuh"
+#include "sprout_kernels.cuh"
+
+namespace sprout {
+
+constexpr uint32_t kGuard = 0x80008000u;
+constexpr int kPrepWarps = 4;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// ---------------------------------------------------------------------------
+// prep: one warp per segment.  Validates the segment's offsets, merges the
+// nonzero thresholds of its valid cells into sorted distinct keys, and for
+// each valid cell the first bin of levels 1..n-1 (count-and-clamp rule).
+__global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(const __grid_constant__ SimArgs a) {
+    extern __shared__ uint32_t prep_smem[];
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    uint32_t *buf = prep_smem + (size_t)warp * 2 * (a.sort_cap > 0 ? a.sort_cap : 1);
+    uint32_t *keys = buf + (a.sort_cap > 0 ? a.sort_cap : 1);
+    const int n = a.n, X = a.X;
+    const int nt = n - 1;
+
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *a.queue = 0u;
+        *a.trace_status = 0u;
+    }
+    const int64_t gw = (int64_t)blockIdx.x * kPrepWarps + warp;
+    const int64_t nwarps = (int64_t)gridDim.x * kPrepWarps;
+    for (int64_t sl = gw; sl < a.n_segments; sl += nwarps) {
+        const int64_t s0 = a.seg_offsets[sl], s1 = a.seg_offsets[sl + 1];
+        if (!(s0 >= 0 && s0 <= s1 && s1 <= a.n_requests && (s1 - s0) < (int64_t)0xFFFFFFFFll)) {
+            if (lane == 0) a.seg_meta[sl] = -2;
+            continue;
+        }
+        if (a.kcap < 0 || nt == 0) {
+            if (lane == 0) a.seg_meta[sl] = (a.kcap < 0) ? -1 : 0;
+            continue;
+        }
+        const int M = X * nt;
+        const int cap = a.sort_cap;
+        // gather nonzero thresholds of valid cells (0 = empty slot)
+        for (int idx = lane; idx < cap; idx += 32) {
+            uint32_t v = 0u;
+            if (idx < M) {
+                const int64_t cell = sl * X + idx / nt;
+                if (a.cell_status[cell] == SPROUT_CELL_OK) v = a.threshold[cell * nt + idx % nt];
+            }
+            buf[idx] = v;
+        }
+        __syncwarp();
+        // bitonic sort ascending
+        for (int k = 2; k <= cap; k <<= 1) {
+            for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                for (int i = lane; i < cap; i += 32) {
+                    const int ixj = i ^ jj;
+                    if (ixj > i) {
+                        const uint32_t u = buf[i], v = buf[ixj];
+                        const bool up = (i & k) == 0;
+                        if ((u > v) == up) { buf[i] = v; buf[ixj] = u; }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        // compact distinct nonzero keys
+        int K = 0;
+        for (int base = 0; base < cap; base += 32) {
+            const int i = base + lane;
+            const uint32_t v = buf[i];
+            const bool first = v != 0u && (i == 0 || buf[i - 1] != v);
+            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, first);
+            const int rank = K + __popc(bal & ((1u << lane) - 1u));
+            if (first) keys[rank] = v;
+            K += __popc(bal);
+        }
+        __syncwarp();
+        if (K > a.kcap) {
+            if (lane == 0) a.seg_meta[sl] = -1;
+            continue;
+        }
+        for (int i = lane; i < K; i += 32) a.seg_keys[sl * a.kcap + i] = keys[i] - 1u;
+        // per valid cell: first bin of each level L >= 1
+        for (int j = lane; j < X; j += 32) {
+            const int64_t cell = sl * X + j;
+            if (a.cell_status[cell] != SPROUT_CELL_OK) continue;
+            const int ml = a.max_level[cell];
+            uint32_t pos[kMaxLevels];
+            for (int i = 0; i < nt; ++i) {
+                const uint32_t t = a.threshold[cell * nt + i];
+                uint32_t ps = 0;
+                if (t != 0u) {   // 1 + index of t in keys (binary search)
+                    int lo = 0, hi = K - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (keys[mid] < t) lo = mid + 1; else hi = mid;
+                    }
+                    ps = (uint32_t)lo + 1u;
+                }
+                pos[i] = ps;
+            }
+            for (int i = 1; i < nt; ++i) {   // insertion sort (nt <= 7)
+                const uint32_t v = pos[i];
+                int k = i - 1;
+                while (k >= 0 && pos[k] > v) { pos[k + 1] = pos[k]; --k; }
+                pos[k + 1] = v;
+            }
+            for (int L = 1; L <= nt; ++L) {
+                const uint32_t bnd = (L <= ml) ? pos[L - 1] : (uint32_t)(K + 1);
+                a.seg_bnd[cell * nt + (L - 1)] = (uint16_t)bnd;
+            }
+        }
+        if (lane == 0) a.seg_meta[sl] = K;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// streaming kernel
+
+template <int N>
+struct Words {
+    static constexpr int NW = (N + 2) / 2;   // 16-bit fields: count, tok_0..tok_{N-1}
+};
+
+template <int N, bool FLAGS>
+struct Group {
+    uint4 t[N];
+    uint2 f;
+};
+
+template <int N, bool FLAGS>
+__device__ __forceinline__ void load_group(Group<N, FLAGS> &g, const SimArgs &a, int64_t v) {
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        g.t[i] = __ldcs(reinterpret_cast<const uint4 *>(a.tokens + (size_t)i * a.pitch) + v);
+    if (FLAGS) g.f = __ldcs(reinterpret_cast<const uint2 *>(a.flags) + v);
+}
+
+// 32-bit word of level plane i holding requests 2(k/2), 2(k/2)+1 of a group
+template <int N, bool FLAGS>
+__device__ __forceinline__ uint32_t plane_word(const Group<N, FLAGS> &g, int i, int k) {
+    const uint4 &u = g.t[i];
+    return (k >> 1) == 0 ? u.x : (k >> 1) == 1 ? u.y : (k >> 1) == 2 ? u.z : u.w;
+}
+
+__device__ __forceinline__ uint32_t half16(uint32_t w, int k) { return (k & 1) ? (w >> 16) : (w & 0xFFFFu); }
+
+// packed word m of request k: fields 2m (low 16) and 2m+1 (high 16) of
+// (1, tok_0, ..., tok_{N-1}, 0) -- one PRMT per word
+template <int N, bool FLAGS>
+__device__ __forceinline__ uint32_t packed_word(const Group<N, FLAGS> &g, int m, int k) {
+    const uint32_t hi_src = (2 * m + 1 <= N) ? plane_word<N, FLAGS>(g, 2 * m, k) : 0u;
+    if (m == 0) return __byte_perm(1u, hi_src, (k & 1) ? 0x7610u : 0x5410u);
+    const uint32_t lo_src = plane_word<N, FLAGS>(g, 2 * m - 1, k);
+    return __byte_perm(lo_src, hi_src, (k & 1) ? 0x7632u : 0x5410u);
+}
+
+struct WarpSmem {
+    uint32_t *hist;              // [(NC*nb + 1)][nw][32] lane-private packed slots
+    unsigned long long *wide;    // [(NC*nb + 1)][n+1] 64-bit per-entry totals
+    uint32_t *keys;              // [kp] breakpoints - 1, padded with 0xFFFFFFFF
+};
+
+__device__ __forceinline__ WarpSmem carve(uint8_t *base, const SimArgs &a) {
+    WarpSmem w;
+    const int entries = a.NC * a.nb + 1;
+    w.wide = reinterpret_cast<unsigned long long *>(base);
+    size_t off = (size_t)entries * (a.n + 1) * 8;
+    w.hist = reinterpret_cast<uint32_t *>(base + off);
+    off += (size_t)entries * a.nw * 32 * 4;
+    w.keys = reinterpret_cast<uint32_t *>(base + off);
+    return w;
+}
+
+// bin of draw w = #{keys < w}: branchless binary search over P (power of
+// two) padded keys holding (breakpoint - 1)
+__device__ __forceinline__ int find_bin(const uint32_t *keys, int P, uint32_t w) {
+    int pos = 0;
+    for (int step = P >> 1; step > 0; step >>= 1) pos += (keys[pos + step - 1] < w) ? step : 0;
+    return pos;
+}
+
+// histogram entry of request k of a group: draw bin, or the class's pinned
+// bin, offset by class; the discard entry for bad classes / masked requests
+template <bool FLAGS>
+__device__ __forceinline__ int entry_of(int bin, uint2 f, int k, int nb, int NC, bool inr, uint32_t &err) {
+    int entry = bin;
+    if (FLAGS) {
+        const uint32_t fw = (k < 4) ? f.x : f.y;
+        const uint32_t fb = (fw >> (8 * (k & 3))) & 0xFFu;
+        const int cls = (int)((fb >> 1) & 3u);
+        if (fb & 1u) entry = nb - 1;
+        entry += cls * nb;
+        if (cls >= NC) {
+            entry = NC * nb;
+            if (inr) err |= SPROUT_TRACE_BAD_CLASS;
+        }
+    }
+    return inr ? entry : NC * nb;
+}
+
+template <int N>
+__device__ __noinline__ void spill_entry(const WarpSmem &W, int entry, uint32_t lane) {
+    constexpr int NW = Words<N>::NW;
+#pragma unroll
+    for (int m = 0; m < NW; ++m) {
+        uint32_t *slot = W.hist + ((size_t)entry * NW + m) * 32 + lane;
+        const uint32_t v = *slot;
+        *slot = 0u;
+        atomicAdd(&W.wide[(size_t)entry * (N + 1) + 2 * m], (unsigned long long)(v & 0xFFFFu));
+        if (2 * m + 1 <= N) atomicAdd(&W.wide[(size_t)entry * (N + 1) + 2 * m + 1], (unsigned long long)(v >> 16));
+    }
+}
+
+// A group holding a token >= 2^15 (would overflow the packed fields): add
+// its requests straight into the 64-bit accumulators.
+template <int N, bool FLAGS>
+__device__ __noinline__ void careful_group(const Group<N, FLAGS> &g, const uint32_t (&w)[8], int lo, int hi,
+                                           const SimArgs &a, const WarpSmem &W, int P, uint32_t &err) {
+    for (int k = 0; k < 8; ++k) {
+        const bool inr = k >= lo && k < hi;
+        const int entry = entry_of<FLAGS>(find_bin(W.keys, P, w[k]), g.f, k, a.nb, a.NC, inr, err);
+        if (entry == a.NC * a.nb) continue;
+        unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
+        atomicAdd(&wr[0], 1ull);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            uint32_t pw = 0;
+#pragma unroll
+            for (int kk = 0; kk < 8; kk += 2)
+                if ((k >> 1) == (kk >> 1)) pw = plane_word<N, FLAGS>(g, i, kk);
+            atomicAdd(&wr[1 + i], (unsigned long long)half16(pw, k));
+        }
+    }
+}
+
+// One group of 8 requests (local requests 8v..8v+7); requests outside
+// [lo, hi) belong to another segment and go to the discard entry.
+template <int N, bool FLAGS, bool FULL>
+__device__ __forceinline__ void process_group(const Group<N, FLAGS> &g, int64_t v, int lo, int hi,
+                                              const SimArgs &a, const WarpSmem &W, int P, uint32_t &err) {
+    constexpr int NW = Words<N>::NW;
+    const uint32_t lane = lane_id();
+
+    // selection draws of the 8 requests (reading L10): counter (g>>2, 0, 0)
+    const uint64_t blk = (a.first_request + (uint64_t)v * 8u) >> 2;
+    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+    const Philox4 d0 = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, k0, k1);
+    const Philox4 d1 = philox4x32_10((uint32_t)(blk + 1), (uint32_t)((blk + 1) >> 32), 0u, 0u, k0, k1);
+    const uint32_t w[8] = {d0.v[0], d0.v[1], d0.v[2], d0.v[3], d1.v[0], d1.v[1], d1.v[2], d1.v[3]};
+
+    uint32_t big = 0u;
+#pragma unroll
+    for (int i = 0; i < N; ++i) big |= g.t[i].x | g.t[i].y | g.t[i].z | g.t[i].w;
+    if (big & kGuard) {
+        careful_group<N, FLAGS>(g, w, lo, hi, a, W, P, err);
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const bool inr = FULL || (k >= lo && k < hi);
+        const int entry = entry_of<FLAGS>(find_bin(W.keys, P, w[k]), g.f, k, a.nb, a.NC, inr, err);
+        uint32_t *slot = W.hist + (size_t)entry * NW * 32 + lane;
+        uint32_t acc = 0u;
+#pragma unroll
+        for (int m = 0; m < NW; ++m) {
+            const uint32_t nv = slot[m * 32] + packed_word<N, FLAGS>(g, m, k);
+            slot[m * 32] = nv;
+            acc |= nv;
+        }
+        if (acc & kGuard) spill_entry<N>(W, entry, lane);
+    }
+}
+
+// Generic path: per request, per cell, compare the draw with the cell's
+// thresholds (count-and-clamp rule) and add into the global per-cell
+// counters with atomics; segment stats go to wide rows [c*nb] / [c*nb+1].
+template <int N, bool FLAGS>
+__device__ __noinline__ void slow_segment(const SimArgs &a, const WarpSmem &W, int64_t sl, int64_t s0, int64_t s1,
+                                          uint32_t &err) {
+    const uint32_t lane = lane_id();
+    const int X = a.X, NC = a.NC;
+    const int64_t cell0 = sl * X;
+    for (int64_t i = lane; i < (int64_t)X * NC * N; i += 32) {
+        a.cnt[cell0 * NC * N + i] = 0ull;
+        a.tok[cell0 * NC * N + i] = 0ull;
+    }
+    __syncwarp();
+    for (int64_t r = s0 + lane; r < s1; r += 32) {
+        const uint64_t gidx = a.first_request + (uint64_t)r;
+        const uint64_t blk = gidx >> 2;
+        const Philox4 d = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, (uint32_t)a.seed,
+                                        (uint32_t)(a.seed >> 32));
+        const uint32_t w = d.v[gidx & 3u];
+        int cls = 0;
+        bool pinned = false;
+        if (FLAGS) {
+            const uint8_t f = a.flags[r];
+            pinned = f & 1u;
+            cls = (f >> 1) & 3;
+        }
+        if (cls >= NC) {
+            err |= SPROUT_TRACE_BAD_CLASS;
+            continue;
+        }
+        unsigned long long *wr = W.wide + (size_t)(cls * a.nb) * (N + 1);
+        atomicAdd(&wr[0], 1ull);
+        for (int i = 0; i < N; ++i) atomicAdd(&wr[1 + i], (unsigned long long)a.tokens[(size_t)i * a.pitch + r]);
+        if (pinned) atomicAdd(&W.wide[(size_t)(cls * a.nb + 1) * (N + 1)], 1ull);
+        for (int j = 0; j < X; ++j) {
+            const int64_t cell = cell0 + j;
+            if (a.cell_status[cell] != SPROUT_CELL_OK) continue;
+            int L = 0;
+            if (!pinned) {
+                int c = 0;
+                for (int i = 0; i + 1 < N; ++i) c += (w >= a.threshold[cell * (N - 1) + i]) ? 1 : 0;
+                const int ml = a.max_level[cell];
+                L = c < ml ? c : ml;
+            }
+            atomicAdd(reinterpret_cast<unsigned long long *>(&a.cnt[(cell * NC + cls) * N + L]), 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long *>(&a.tok[(cell * NC + cls) * N + L]),
+                      (unsigned long long)a.tokens[(size_t)L * a.pitch + r]);
+        }
+    }
+    err |= SPROUT_TRACE_SLOW_PATH;
+    __syncwarp();
+}
+
+// Segment statistics and the Base counterfactual (every request at L0,
+// P:366): counts and token sums per class, fp64 Base energy/time/carbon
+// (Eq. 1) and quality.  Fast path: totals = row `tot_row` (prefix total) +
+// the pinned row; slow path: totals in row 0, pinned count in row 1.
+template <int N>
+__device__ __noinline__ void write_seg_stats(const SimArgs &a, const WarpSmem &W, int64_t sl, double kp, double q0,
+                                             int tot_row, int pin_row, bool fast, const CostConst &cost) {
+    if (lane_id() != 0) return;
+    const int NC = a.NC, nb = a.nb;
+    double bE = 0.0, bT = 0.0, m = 0.0;
+    for (int c = 0; c < NC; ++c) {
+        const unsigned long long *tr = W.wide + (size_t)(c * nb + tot_row) * (N + 1);
+        const unsigned long long *pr = W.wide + (size_t)(c * nb + pin_row) * (N + 1);
+        const unsigned long long mc = tr[0] + (fast ? pr[0] : 0ull);
+        a.seg_count[sl * NC + c] = mc;
+        a.seg_pinned[sl * NC + c] = pr[0];
+        unsigned long long t0 = 0;
+        for (int i = 0; i < N; ++i) {
+            const unsigned long long t = tr[1 + i] + (fast ? pr[1 + i] : 0ull);
+            a.seg_tok[(sl * NC + c) * N + i] = t;
+            if (i == 0) t0 = t;
+        }
+        bE += (double)mc * cost.ef[c][0] + (double)t0 * cost.et[c][0];
+        bT += (double)mc * cost.pf[c][0] + (double)t0 * cost.pt[c][0];
+        m += (double)mc;
+    }
+    a.seg_base[sl * 4 + 0] = bE;
+    a.seg_base[sl * 4 + 1] = bT;
+    a.seg_base[sl * 4 + 2] = kp * bE + a.k1 * bT;
+    a.seg_base[sl * 4 + 3] = m * q0;
+}
+
+__device__ __forceinline__ void zero_cell(const SimArgs &a, int64_t cell, int NCN) {
+    for (int i = 0; i < NCN; ++i) { a.cnt[cell * NCN + i] = 0ull; a.tok[cell * NCN + i] = 0ull; }
+    a.energy[cell] = 0.0; a.time_s[cell] = 0.0; a.carbon[cell] = 0.0; a.quality[cell] = 0.0;
+}
+
+// Per-cell integer statistics (from the histogram prefix sums, or from the
+// slow path's global counters) and the closed-form fp64 totals of Eq. 1.
+template <int N>
+__device__ __noinline__ void cell_epilogue(const SimArgs &a, const WarpSmem &W, int64_t sl, int K, double kp,
+                                           const double *qrow, bool fast, const CostConst &cost) {
+    const int NC = a.NC, nb = a.nb;
+    for (int j = lane_id(); j < a.X; j += 32) {
+        const int64_t cell = sl * a.X + j;
+        if (a.cell_status[cell] != SPROUT_CELL_OK) {
+            zero_cell(a, cell, NC * N);
+            continue;
+        }
+        int bnd[N + 1];
+        bnd[0] = 0;
+        bnd[N] = K + 1;
+        if (fast)
+#pragma unroll
+            for (int L = 1; L < N; ++L) bnd[L] = a.seg_bnd[cell * (N - 1) + (L - 1)];
+        double E = 0.0, T = 0.0, Q = 0.0;
+        for (int c = 0; c < NC; ++c) {
+            const unsigned long long *pre = W.wide + (size_t)(c * nb) * (N + 1);
+            const unsigned long long *pin = W.wide + (size_t)(c * nb + nb - 1) * (N + 1);
+#pragma unroll
+            for (int L = 0; L < N; ++L) {
+                unsigned long long cn, tk;
+                uint64_t *pc = &a.cnt[(cell * NC + c) * N + L];
+                uint64_t *pt = &a.tok[(cell * NC + c) * N + L];
+                if (fast) {
+                    cn = pre[(size_t)bnd[L + 1] * (N + 1)] - pre[(size_t)bnd[L] * (N + 1)];
+                    tk = pre[(size_t)bnd[L + 1] * (N + 1) + 1 + L] - pre[(size_t)bnd[L] * (N + 1) + 1 + L];
+                    if (L == 0) { cn += pin[0]; tk += pin[1]; }
+                    *pc = cn;
+                    *pt = tk;
+                } else {
+                    cn = __ldcg(reinterpret_cast<const unsigned long long *>(pc));
+                    tk = __ldcg(reinterpret_cast<const unsigned long long *>(pt));
+                }
+                const double n_ = (double)cn, t_ = (double)tk;
+                E += n_ * cost.ef[c][L] + t_ * cost.et[c][L];
+                T += n_ * cost.pf[c][L] + t_ * cost.pt[c][L];
+                Q += n_ * qrow[L];
+            }
+        }
+        a.energy[cell] = E;
+        a.time_s[cell] = T;
+        a.carbon[cell] = kp * E + a.k1 * T;
+        a.quality[cell] = Q;
+    }
+}
+
+// Lane-private slots -> 64-bit per-entry totals, then the exclusive prefix
+// over draw bins 0..K+1 per (class, field).
+template <int N>
+__device__ __noinline__ void readout(const SimArgs &a, const WarpSmem &W, int K) {
+    constexpr int NW = Words<N>::NW;
+    const uint32_t lane = lane_id();
+    const int NC = a.NC, nb = a.nb;
+    const int used = K + 2;   // draw bins 0..K and the pinned bin
+    for (int e = lane; e < NC * used; e += 32) {
+        const int c = e / used, b = e % used;
+        const int entry = c * nb + (b <= K ? b : nb - 1);
+        unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
+#pragma unroll
+        for (int m = 0; m < NW; ++m) {
+            uint32_t *row = W.hist + ((size_t)entry * NW + m) * 32;
+            uint32_t slo = 0u, shi = 0u;
+#pragma unroll 8
+            for (int q = 0; q < 32; ++q) {
+                const int idx = (q + (int)lane) & 31;   // rotated: conflict-free
+                const uint32_t val = row[idx];
+                row[idx] = 0u;
+                slo += val & 0xFFFFu;
+                shi += val >> 16;
+            }
+            wr[2 * m] += slo;
+            if (2 * m + 1 <= N) wr[2 * m + 1] += shi;
+        }
+    }
+    for (int i = lane; i < NW * 32; i += 32) W.hist[(size_t)(NC * nb) * NW * 32 + i] = 0u;   // discard entry
+    for (int i = lane; i < N + 1; i += 32) W.wide[(size_t)(NC * nb) * (N + 1) + i] = 0ull;
+    __syncwarp();
+    for (int e = lane; e < NC * (N + 1); e += 32) {
+        const int c = e / (N + 1), f = e % (N + 1);
+        unsigned long long run = 0ull;
+        for (int b = 0; b <= K + 1; ++b) {
+            unsigned long long *pt = &W.wide[(size_t)(c * nb + b) * (N + 1) + f];
+            const unsigned long long v2 = *pt;
+            *pt = run;
+            run += v2;
+        }
+    }
+    __syncwarp();
+}
+
+template <int N, bool FLAGS>
+__device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem &W, int64_t s0, int64_t s1, int P,
+                                               uint32_t &err) {
+    if (s1 <= s0) return;
+    const int64_t vfirst = s0 >> 3, vlast = (s1 - 1) >> 3;
+    int64_t v = vfirst + lane_id();
+    constexpr int D = N <= 4 ? 2 : 1;   // groups in flight per lane beyond the current pair
+    Group<N, FLAGS> cur[D], nxt[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+        if (v + 32 * d <= vlast) load_group<N, FLAGS>(cur[d], a, v + 32 * d);
+    for (; v <= vlast; v += 32 * D) {
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            if (v + 32 * (D + d) <= vlast) load_group<N, FLAGS>(nxt[d], a, v + 32 * (D + d));
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const int64_t vv = v + 32 * d;
+            if (vv <= vlast) {
+                const int64_t r0 = vv * 8;
+                const int lo = (int)(s0 > r0 ? s0 - r0 : 0);
+                const int hi = (int)(s1 - r0 < 8 ? s1 - r0 : 8);
+                if (lo == 0 && hi == 8)
+                    process_group<N, FLAGS, true>(cur[d], vv, 0, 8, a, W, P, err);
+                else
+                    process_group<N, FLAGS, false>(cur[d], vv, lo, hi, a, W, P, err);
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < D; ++d) cur[d] = nxt[d];
+    }
+}
+
+template <int N, bool FLAGS>
+__global__ void __launch_bounds__(512, 1) trace_kernel(const __grid_constant__ SimArgs a) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ CostConst cost;   // per-launch coefficients (dynamic [class][level] indexing)
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    constexpr int NW = Words<N>::NW;
+    const WarpSmem W = carve(smem + (size_t)warp * a.warp_smem, a);
+    const int NC = a.NC, nb = a.nb, X = a.X;
+    const int entries = NC * nb + 1;
+    for (int i = threadIdx.x; i < (int)(sizeof(CostConst) / 8); i += blockDim.x)
+        reinterpret_cast<double *>(&cost)[i] = reinterpret_cast<const double *>(&a.cost)[i];
+    for (int i = lane; i < entries * NW * 32; i += 32) W.hist[i] = 0u;
+    for (int i = lane; i < entries * (N + 1); i += 32) W.wide[i] = 0ull;
+    __syncthreads();
+
+    uint32_t err = 0u;
+    for (;;) {
+        int64_t sl = 0;
+        if (lane == 0) sl = (int64_t)atomicAdd(a.queue, 1u);
+        sl = __shfl_sync(0xFFFFFFFFu, sl, 0);
+        if (sl >= a.n_segments) break;
+        const int64_t s = a.first_segment + sl;
+        const int meta = a.seg_meta[sl];
+        const double *qrow = a.q + (a.profile_per_interval ? s : s / a.T) * N;
+        const double kp = a.k0[s] * a.pue;
+
+        if (meta == -2) {   // invalid offsets: segment skipped, outputs zero
+            err |= SPROUT_TRACE_BAD_OFFSETS;
+            for (int j = lane; j < X; j += 32) zero_cell(a, sl * X + j, NC * N);
+            for (int i = lane; i < NC; i += 32) { a.seg_count[sl * NC + i] = 0ull; a.seg_pinned[sl * NC + i] = 0ull; }
+            for (int i = lane; i < NC * N; i += 32) a.seg_tok[sl * NC * N + i] = 0ull;
+            if (lane < 4) a.seg_base[sl * 4 + lane] = 0.0;
+            continue;
+        }
+        const int64_t s0 = a.seg_offsets[sl], s1 = a.seg_offsets[sl + 1];
+        if (meta == -1) {
+            slow_segment<N, FLAGS>(a, W, sl, s0, s1, err);
+            cell_epilogue<N>(a, W, sl, 0, kp, qrow, false, cost);
+            __syncwarp();
+            write_seg_stats<N>(a, W, sl, kp, qrow[0], 0, 1, false, cost);
+            __syncwarp();
+            for (int e = lane; e < NC * 2 * (N + 1); e += 32) {
+                const int c = e / (2 * (N + 1)), rem = e % (2 * (N + 1));
+                W.wide[(size_t)(c * nb + rem / (N + 1)) * (N + 1) + rem % (N + 1)] = 0ull;
+            }
+            __syncwarp();
+            continue;
+        }
+        const int K = meta;
+        int P = 1;
+        while (P < K + 1) P <<= 1;
+        for (int i = lane; i < P; i += 32) W.keys[i] = i < K ? a.seg_keys[sl * a.kcap + i] : 0xFFFFFFFFu;
+        __syncwarp();
+        stream_segment<N, FLAGS>(a, W, s0, s1, P, err);
+        __syncwarp();
+        readout<N>(a, W, K);
+        cell_epilogue<N>(a, W, sl, K, kp, qrow, true, cost);
+        __syncwarp();
+        write_seg_stats<N>(a, W, sl, kp, qrow[0], K + 1, nb - 1, true, cost);
+        __syncwarp();
+        // clear the rows used by this segment: draw bins 0..K+1 and the pinned bin
+        for (int e = lane; e < NC * (K + 3) * (N + 1); e += 32) {
+            const int c = e / ((K + 3) * (N + 1));
+            const int rem = e % ((K + 3) * (N + 1));
+            const int b = rem / (N + 1), f = rem % (N + 1);
+            W.wide[(size_t)(c * nb + (b <= K + 1 ? b : nb - 1)) * (N + 1) + f] = 0ull;
+        }
+        __syncwarp();
+    }
+    err = __reduce_or_sync(0xFFFFFFFFu, err);
+    if (lane == 0 && err) atomicOr(a.trace_status, err);
+}
+
+// ---------------------------------------------------------------------------
+// verify mode (levels_out): the level of every request in every cell of its
+// segment, from the same draw, the same breakpoint keys and the same
+// per-cell bin boundaries the streaming kernel aggregates over (or, for
+// slow segments, directly from the thresholds).  One warp per segment.
+template <int N>
+__global__ void __launch_bounds__(256) levels_kernel(const __grid_constant__ SimArgs a) {
+    const uint32_t lane = lane_id();
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t sl = gw; sl < a.n_segments; sl += nw) {
+        const int meta = a.seg_meta[sl];
+        if (meta == -2) continue;
+        const int64_t s0 = a.seg_offsets[sl], s1 = a.seg_offsets[sl + 1];
+        for (int64_t r = s0 + lane; r < s1; r += 32) {
+            const uint64_t gidx = a.first_request + (uint64_t)r;
+            const uint64_t blk = gidx >> 2;
+            const Philox4 d = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, (uint32_t)a.seed,
+                                            (uint32_t)(a.seed >> 32));
+            const uint32_t w = d.v[gidx & 3u];
+            bool pinned = false, bad = false;
+            if (a.flags) {
+                const uint8_t f = a.flags[r];
+                pinned = f & 1u;
+                bad = ((f >> 1) & 3) >= a.NC;
+            }
+            int bin = 0;
+            if (meta >= 0) {
+                const uint32_t *keys = a.seg_keys + sl * a.kcap;
+                for (int k = 0; k < meta; ++k) bin += (keys[k] < w) ? 1 : 0;
+            }
+            for (int j = 0; j < a.X; ++j) {
+                const int64_t cell = sl * a.X + j;
+                uint8_t L = 0xFF;
+                if (!bad && a.cell_status[cell] == SPROUT_CELL_OK) {
+                    L = 0;
+                    if (!pinned) {
+                        if (meta >= 0) {
+                            for (int l = 1; l < N; ++l)
+                                if ((int)a.seg_bnd[cell * (N - 1) + (l - 1)] <= bin) L = (uint8_t)l;
+                        } else {
+                            int c = 0;
+                            for (int i = 0; i + 1 < N; ++i) c += (w >= a.threshold[cell * (N - 1) + i]) ? 1 : 0;
+                            const int ml = a.max_level[cell];
+                            L = (uint8_t)(c < ml ? c : ml);
+                        }
+                    }
+                }
+                a.levels_out[(size_t)j * a.pitch + r] = L;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+// breakpoint slots per segment in the workspace: the fast path's nominal
+// capacity (independent of the class count and of the shared-memory fit)
+static int nominal_kcap(int n, int X) {
+    const long M = (long)X * (n - 1);
+    return (n == 1) ? 0 : (int)((M < (long)X + 1) ? M : (long)X + 1);
+}
+
+bool make_sim_plan(int n, int X, int NC, SimPlan *plan) {
+    SimPlan p{};
+    p.n = n; p.X = X; p.NC = NC;
+    p.nw = (n + 2) / 2;
+    const long M = (long)X * (n - 1);
+    int kcap = nominal_kcap(n, X);
+    p.sort_cap = 0;
+    if (M > 0) {
+        long c = 1;
+        while (c < M) c <<= 1;
+        p.sort_cap = (int)(c < 32 ? 32 : c);
+    }
+    if (p.sort_cap > 4096) kcap = -1;     // too many thresholds to merge per warp: generic path
+    auto per_warp = [&](int kc, int *nb_out, int *kp_out) {
+        const int kk = kc < 0 ? 0 : kc;
+        const int nb = kk + 3;
+        int kp = 1;
+        while (kp < kk + 1) kp <<= 1;
+        const size_t entries = (size_t)NC * nb + 1;
+        size_t bytes = entries * (n + 1) * 8 + entries * p.nw * 32 * 4 + (size_t)kp * 4;
+        *nb_out = nb;
+        *kp_out = kp;
+        return (bytes + 15) & ~(size_t)15;
+    };
+    const size_t smem_cap = 227 * 1024 - 2048;   // leave room for the static cost table
+    int nb, kp;
+    size_t bytes = per_warp(kcap, &nb, &kp);
+    if (kcap >= 0 && bytes > smem_cap) {
+        kcap = -1;
+        bytes = per_warp(kcap, &nb, &kp);
+    }
+    p.kcap = kcap;
+    p.nb = nb;
+    p.kp = kp;
+    p.warp_smem = bytes;
+    int wpc = (int)(smem_cap / bytes);
+    if (wpc > 16) wpc = 16;
+    if (wpc < 1) return false;
+    p.warps_per_cta = wpc;
+    *plan = p;
+    return true;
+}
+
+size_t sim_workspace_bytes(const SimPlan &p, int64_t n_segments) {
+    const int kc = nominal_kcap(p.n, p.X);
+    size_t b = 256;                                             // queue
+    b += ((size_t)n_segments * 4 + 255) & ~(size_t)255;         // seg_meta
+    b += ((size_t)n_segments * kc * 4 + 255) & ~(size_t)255;   // seg_keys
+    const size_t cells = (size_t)n_segments * p.X;
+    b += (cells * (p.n > 1 ? p.n - 1 : 0) * 2 + 255) & ~(size_t)255;  // seg_bnd
+    return b;
+}
+
+template <int N, bool FLAGS>
+static cudaError_t launch_trace_t(SimArgs &a, const SimPlan &plan, cudaStream_t stream) {
+    const int threads = plan.warps_per_cta * 32;
+    const size_t smem = plan.warp_smem * plan.warps_per_cta;
+    auto kern = trace_kernel<N, FLAGS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t grid = (int64_t)sms * per_sm;
+    const int64_t need = (a.n_segments + plan.warps_per_cta - 1) / plan.warps_per_cta;
+    if (grid > need) grid = need > 0 ? need : 1;
+    kern<<<(unsigned)grid, threads, smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t launch_n(SimArgs &a, const SimPlan &plan, cudaStream_t stream, int *launches) {
+    cudaError_t e = a.flags ? launch_trace_t<N, true>(a, plan, stream) : launch_trace_t<N, false>(a, plan, stream);
+    if (e != cudaSuccess) return e;
+    ++*launches;
+    if (a.levels_out) {
+        int64_t blocks = (a.n_segments * 32 + 255) / 256;
+        if (blocks > 148 * 32) blocks = 148 * 32;
+        levels_kernel<N><<<(unsigned)blocks, 256, 0, stream>>>(a);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        ++*launches;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStream_t stream, int *launches) {
+    uint8_t *w = static_cast<uint8_t *>(ws);
+    a.queue = reinterpret_cast<uint32_t *>(w);
+    size_t off = 256;
+    a.seg_meta = reinterpret_cast<int32_t *>(w + off);
+    off += ((size_t)a.n_segments * 4 + 255) & ~(size_t)255;
+    a.seg_keys = reinterpret_cast<uint32_t *>(w + off);
+    const int kc = nominal_kcap(plan.n, plan.X);
+    off += ((size_t)a.n_segments * kc * 4 + 255) & ~(size_t)255;
+    a.seg_bnd = reinterpret_cast<uint16_t *>(w + off);
+    a.kcap = plan.kcap < 0 ? -1 : kc;
+    a.nb = plan.nb;
+    a.nw = plan.nw;
+    a.kp = plan.kp;
+    a.sort_cap = plan.sort_cap;
+    a.warp_smem = plan.warp_smem;
+
+    // prep (also resets the queue and trace_status)
+    {
+        int64_t blocks = (a.n_segments + kPrepWarps - 1) / kPrepWarps;
+        if (blocks > 148 * 16) blocks = 148 * 16;
+        if (blocks < 1) blocks = 1;
+        const size_t smem = (size_t)kPrepWarps * 2 * (plan.sort_cap > 0 ? plan.sort_cap : 1) * 4;
+        cudaError_t e = cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        prep_kernel<<<(unsigned)blocks, 32 * kPrepWarps, smem, stream>>>(a);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        ++*launches;
+    }
+    if (a.n_segments == 0) return cudaSuccess;
+    switch (a.n) {
+        case 1: return launch_n<1>(a, plan, stream, launches);
+        case 2: return launch_n<2>(a, plan, stream, launches);
+        case 3: return launch_n<3>(a, plan, stream, launches);
+        case 4: return launch_n<4>(a, plan, stream, launches);
+        case 5: return launch_n<5>(a, plan, stream, launches);
+        case 6: return launch_n<6>(a, plan, stream, launches);
+        case 7: return launch_n<7>(a, plan, stream, launches);
+        case 8: return launch_n<8>(a, plan, stream, launches);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace sprout

@@ -1,0 +1,114 @@
+"""Device-side orchestration of one rank's sweep: allocate the C-ABI
+buffers as torch tensors, put the trace on the device (uploaded from the host
+or generated in place by the harness-only generator kernel), and call the
+three hot-path entry points.  Marshalling only -- no arithmetic of the method.
+
+Inputs are duck-typed (any objects with the attributes of synth.Problem,
+synth.CostModel, synth.TraceSpec and synth.Shard), so the product package does
+not depend on the input generator.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import sprout as S
+
+
+def _pitch(n_requests: int) -> int:
+    return max(8, ((n_requests + 7) // 8) * 8)
+
+
+class Sweep:
+    """One rank's slice: segments [shard.first_segment, +n_segments) and the
+    local requests [shard.first_request, +n_requests)."""
+
+    def __init__(self, prob, cost, shard, device, spec=None, tokens: Optional[np.ndarray] = None,
+                 flags: Optional[np.ndarray] = None, has_flags: Optional[bool] = None):
+        self.device = torch.device(device)
+        self.prob_host = prob
+        self.dp = S.DeviceProblem.from_host(prob, self.device, shard.first_segment, shard.n_segments)
+        self.sol = S.Solution.empty(self.dp)
+        self.cost = S.cost_model(cost)
+        self.n_classes = int(cost.n_classes)
+        self.totals = S.Totals.empty(self.dp, self.n_classes)
+        n = prob.n
+        pitch = _pitch(shard.n_requests)
+        seg = torch.as_tensor(np.ascontiguousarray(shard.seg_offsets, np.int64)).to(self.device)
+        if tokens is not None:
+            tok = np.zeros((n, pitch), np.uint16)
+            tok[:, :tokens.shape[1]] = tokens[:, :pitch]
+            tok_t = torch.from_numpy(tok.view(np.int16)).to(self.device)
+            fl_t = None
+            if flags is not None:
+                fl = np.zeros(pitch, np.uint8)
+                fl[:flags.shape[0]] = flags[:pitch]
+                fl_t = torch.from_numpy(fl).to(self.device)
+        else:
+            assert spec is not None, "need a TraceSpec to generate the trace on the device"
+            use_flags = spec.has_flags if has_flags is None else has_flags
+            tok_t = torch.empty((n, pitch), dtype=torch.int16, device=self.device)
+            fl_t = torch.empty(pitch, dtype=torch.uint8, device=self.device) if use_flags else None
+            self.generate(spec, shard, tok_t, fl_t)
+        self.trace = S.DeviceTrace(shard.n_requests, shard.first_request, seg, tok_t, fl_t)
+        self.ws = S.workspace(S.workspace_bytes(self.dp, self.trace), self.device)
+        self.rws = S.workspace(S.reduce_workspace_bytes(self.dp), self.device)
+        K = S.group_stat_count(n)
+        self.group = torch.zeros((prob.R + 1, prob.X, K), dtype=torch.float64, device=self.device)
+        self.levels = None
+
+    def generate(self, spec, shard, tok_t, fl_t, stream=None):
+        q0 = torch.from_numpy(np.ascontiguousarray(spec.q0_table, np.uint16).view(np.int16)).to(self.device)
+        rt = torch.from_numpy(np.ascontiguousarray(spec.ratio_table, np.uint16).view(np.int16)).to(self.device)
+        self._gen_tables = (q0, rt)
+        gen = S.TraceGenerator(int(spec.gen_seed) & 0xFFFFFFFFFFFFFFFF, int(shard.first_request),
+                               int(shard.n_requests), int(spec.n_levels), int(spec.n_classes),
+                               int(spec.pin_thresh) if fl_t is not None else 0, 0, q0.data_ptr(), rt.data_ptr())
+        S.generate_trace(gen, tok_t, fl_t, stream)
+
+    # the three hot-path steps
+    def solve(self, stream=None):
+        S.solve_directives(self.dp, self.sol, stream)
+
+    def simulate(self, levels: bool = False, stream=None):
+        lv = None
+        if levels:
+            if self.levels is None:
+                self.levels = torch.full((self.dp.X, self.trace.pitch), 0xFF, dtype=torch.uint8, device=self.device)
+            lv = self.levels
+        S.simulate_trace(self.dp, self.sol, self.trace, self.cost, self.totals, self.ws, lv, stream)
+
+    def reduce(self, stream=None):
+        S.reduce_totals(self.dp, self.sol, self.totals, self.n_classes, self.group, self.rws, stream)
+
+    def step(self, stream=None):
+        self.solve(stream)
+        self.simulate(False, stream)
+        self.reduce(stream)
+
+    # host views (for tests)
+    def host(self) -> dict:
+        t = self.totals
+        out = {k: getattr(t, k).cpu().numpy() for k in ("energy", "time", "carbon", "quality", "seg_base")}
+        for k in ("cnt", "tok", "seg_count", "seg_pinned", "seg_tok"):
+            out[k] = getattr(t, k).cpu().numpy().view(np.uint64)
+        out["trace_status"] = int(t.trace_status.cpu().numpy().view(np.uint32)[0])
+        sol = self.sol
+        out["x"] = sol.x.cpu().numpy()
+        out["objective"] = sol.objective.cpu().numpy()
+        out["q_lb"] = sol.q_lb.cpu().numpy()
+        out["vertex"] = sol.vertex.cpu().numpy()
+        out["threshold"] = sol.thresholds_u32()
+        out["max_level"] = sol.max_level.cpu().numpy()
+        out["cell_status"] = sol.cell_status.cpu().numpy()
+        out["group"] = self.group.cpu().numpy()
+        if self.levels is not None:
+            out["levels"] = self.levels.cpu().numpy()
+        return out
+
+    def trace_host(self):
+        tok = self.trace.tokens.cpu().numpy().view(np.uint16)
+        fl = self.trace.flags.cpu().numpy() if self.trace.flags is not None else None
+        return tok, fl

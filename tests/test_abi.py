@@ -1,0 +1,109 @@
+"""The C-ABI library loads and exports every symbol include/sprout.h declares;
+host-side validation rejects bad arguments before touching a device (CPU)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sprout.h")
+LIB = os.path.join(ROOT, "paper_2403_12900_b200", "libsprout.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sprout_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        from paper_2403_12900_b200 import build
+        build.build()
+    return C.CDLL(LIB)
+
+
+def test_header_declares_the_hot_path():
+    fns = declared_functions()
+    for name in ("sprout_solve_directives", "sprout_simulate_trace", "sprout_reduce_totals"):
+        assert name in fns
+
+
+def test_every_declared_symbol_is_exported(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_binding_covers_every_export():
+    from paper_2403_12900_b200 import sprout as S
+    assert sorted(S.EXPORTS) == declared_functions()
+
+
+def test_struct_layouts_match_header():
+    from paper_2403_12900_b200 import sprout as S
+    # field offsets implied by the C declarations (LP64)
+    assert C.sizeof(S.LpProblem) == 4 + 4 + 8 + 4 + 4 + 7 * 8 + 8 + 8 + 8 + 8
+    assert S.LpProblem.n_intervals.offset == 8 and S.LpProblem.k0.offset == 24
+    assert C.sizeof(S.CostModel) == 16 + 4 * 4 * 8 * 8
+    assert S.CostModel.ef.offset == 16
+    assert C.sizeof(S.Trace) == 48 and C.sizeof(S.CellTotals) == 11 * 8
+    assert C.sizeof(S.TraceGenerator) == 8 + 8 + 8 + 4 + 4 + 4 + 4 + 8 + 8
+
+
+def test_status_strings(lib):
+    lib.sprout_status_string.restype = C.c_char_p
+    assert lib.sprout_status_string(0) == b"ok"
+    assert lib.sprout_status_string(1) == b"invalid argument"
+    lib.sprout_group_stat_count.restype = C.c_int32
+    assert lib.sprout_group_stat_count(3) == 17
+
+
+def _problem(S, **kw):
+    d = dict(n_levels=3, n_regions=1, n_intervals=2, n_xi=1, profile_per_interval=0,
+             k0=16, k0_min=16, k0_max=16, xi=16, e=16, p=16, q=16, k1=0.001, pue=1.2,
+             first_segment=0, n_segments=2)
+    d.update(kw)
+    return S.LpProblem(*[d[f[0]] for f in S.LpProblem._fields_])
+
+
+@pytest.mark.parametrize("field,value", [("n_levels", 0), ("n_levels", 9), ("n_regions", 0), ("n_xi", 0),
+                                         ("n_xi", 5000), ("pue", 0.9), ("pue", float("nan")), ("k1", -1.0),
+                                         ("n_segments", 3), ("first_segment", -1), ("k0", None)])
+def test_host_validation_rejects_without_device(field, value):
+    from paper_2403_12900_b200 import sprout as S
+    P = _problem(S, **{field: value})
+    sol = S.LpSolution(16, 16, 16, 16, 16, 16, 16)
+    st = S._lib.sprout_solve_directives(C.byref(P), C.byref(sol), None)
+    assert st == 1
+    assert S._lib.sprout_workspace_bytes(C.byref(P), None) == 0
+
+
+def test_trace_validation_rejects_without_device():
+    from paper_2403_12900_b200 import sprout as S
+    P = _problem(S)
+    sol = S.LpSolution(16, 16, 16, 16, 16, 16, 16)
+    cost = S.CostModel(); cost.n_classes = 1
+    tot = S.CellTotals(*([16] * 11))
+    for tr in (S.Trace(10, 4, 16, 16, 16, None),       # first_request not a multiple of 8
+               S.Trace(10, 0, 16, 16, 12, None),       # pitch not a multiple of 8
+               S.Trace(20, 0, 16, 16, 16, None),       # pitch < n_requests
+               S.Trace(10, 0, 16, 18, 16, None),       # misaligned tokens
+               S.Trace(10, 0, None, 16, 16, None)):    # no offsets
+        st = S._lib.sprout_simulate_trace(C.byref(P), C.byref(sol), C.byref(tr), C.byref(cost), C.byref(tot),
+                                          None, 256, 1 << 20, None)
+        assert st == 1
+    cost.n_classes = 5
+    st = S._lib.sprout_simulate_trace(C.byref(P), C.byref(sol), C.byref(S.Trace(10, 0, 16, 16, 16, None)),
+                                      C.byref(cost), C.byref(tot), None, 256, 1 << 20, None)
+    assert st == 1
+
+
+def test_workspace_size_monotone():
+    from paper_2403_12900_b200 import sprout as S
+    a = S._lib.sprout_workspace_bytes(C.byref(_problem(S, n_segments=1)), None)
+    b = S._lib.sprout_workspace_bytes(C.byref(_problem(S, n_segments=2)), None)
+    c = S._lib.sprout_workspace_bytes(C.byref(_problem(S, n_xi=64, n_segments=2)), None)
+    assert 0 < a <= b < c
