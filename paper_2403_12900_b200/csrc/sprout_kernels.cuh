@@ -7,6 +7,15 @@
 
 namespace sprout {
 
+// bin lookup table: 2^10 buckets of the 32-bit draw; an entry holds the bin
+// at the bucket start (9 bits), a multi-key flag and the low 22 bits of the
+// bucket's single breakpoint
+constexpr int kLutBits = 10;
+constexpr int kLutBuckets = 1 << kLutBits;
+constexpr int kLutMinKeys = 8;      // fewer keys: level-synchronous binary search
+constexpr int kLutMaxKeys = 511;    // bin field width
+constexpr int kLutMinRequests = 4096;  // shorter segments do not amortise the table build
+
 struct LpArgs {
     int n, X;
     int64_t T, first_segment, n_segments;
@@ -26,6 +35,7 @@ struct SimPlan {
     int nb;            // bins per class in the warp histograms: kcap+1 draw bins, a total slot, the pinned bin
     int nw;            // 32-bit histogram words per entry = ceil((n+1)/2)
     int kp;            // key slots per segment in shared memory (power of two >= kcap+1)
+    int lut;           // bucket lookup table in use (kcap in [kLutMinKeys, kLutMaxKeys])
     int warps_per_cta;
     size_t warp_smem;  // bytes of shared memory per warp
     int ctas;          // persistent grid size
@@ -64,7 +74,9 @@ struct SimArgs {
     uint16_t *seg_bnd;         // [n_segments][X][n-1] first bin of each level >= 1
     // plan
     int kcap, nb, nw, kp, sort_cap;
+    int lut;                   // 1: per-warp bucket table (kLutBuckets entries) for big segments
     size_t warp_smem;
+    uint32_t rk0[10], rk1[10]; // Philox round keys of the selection seed
     CostConst cost;
 };
 

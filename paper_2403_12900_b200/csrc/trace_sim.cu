@@ -142,10 +142,16 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(const __grid_cons
 
 // ---------------------------------------------------------------------------
 // streaming kernel
+//
+// Lane-private histogram entry layout: 16-bit fields packed two per 32-bit
+// word, words grouped in pairs (one 64-bit shared access per pair):
+//   word 0 = tok_0 (low) | count (high);  word m >= 1 = tok_{2m-1} | tok_{2m}.
+// Field f of the 64-bit accumulators ("wide" rows) is 0 = count, 1+i = tok_i.
 
 template <int N>
 struct Words {
-    static constexpr int NW = (N + 2) / 2;   // 16-bit fields: count, tok_0..tok_{N-1}
+    static constexpr int NW = (N + 2) / 2;   // 32-bit words per entry
+    static constexpr int NP = (NW + 1) / 2;  // 64-bit pairs per entry
 };
 
 template <int N, bool FLAGS>
@@ -171,19 +177,23 @@ __device__ __forceinline__ uint32_t plane_word(const Group<N, FLAGS> &g, int i, 
 
 __device__ __forceinline__ uint32_t half16(uint32_t w, int k) { return (k & 1) ? (w >> 16) : (w & 0xFFFFu); }
 
-// packed word m of request k: fields 2m (low 16) and 2m+1 (high 16) of
-// (1, tok_0, ..., tok_{N-1}, 0) -- one PRMT per word
+// packed word m of request k (without the count increment of word 0)
 template <int N, bool FLAGS>
 __device__ __forceinline__ uint32_t packed_word(const Group<N, FLAGS> &g, int m, int k) {
-    const uint32_t hi_src = (2 * m + 1 <= N) ? plane_word<N, FLAGS>(g, 2 * m, k) : 0u;
-    if (m == 0) return __byte_perm(1u, hi_src, (k & 1) ? 0x7610u : 0x5410u);
+    if (m == 0) return half16(plane_word<N, FLAGS>(g, 0, k), k);
     const uint32_t lo_src = plane_word<N, FLAGS>(g, 2 * m - 1, k);
+    const uint32_t hi_src = (2 * m <= N - 1) ? plane_word<N, FLAGS>(g, 2 * m, k) : 0u;
     return __byte_perm(lo_src, hi_src, (k & 1) ? 0x7632u : 0x5410u);
 }
 
+// (low field index, high field index) of word m in the wide rows
+__device__ __forceinline__ int word_lo_field(int m) { return m == 0 ? 1 : 2 * m; }
+__device__ __forceinline__ int word_hi_field(int m) { return m == 0 ? 0 : 2 * m + 1; }
+
 struct WarpSmem {
-    uint32_t *hist;              // [(NC*nb + 1)][nw][32] lane-private packed slots
+    uint2 *hist;                 // [(NC*nb + 1)][np][32] lane-private packed pairs
     unsigned long long *wide;    // [(NC*nb + 1)][n+1] 64-bit per-entry totals
+    uint32_t *lut;               // [kLutBuckets] bin lookup table (if a.lut)
     uint32_t *keys;              // [kp] breakpoints - 1, padded with 0xFFFFFFFF
 };
 
@@ -192,8 +202,10 @@ __device__ __forceinline__ WarpSmem carve(uint8_t *base, const SimArgs &a) {
     const int entries = a.NC * a.nb + 1;
     w.wide = reinterpret_cast<unsigned long long *>(base);
     size_t off = (size_t)entries * (a.n + 1) * 8;
-    w.hist = reinterpret_cast<uint32_t *>(base + off);
-    off += (size_t)entries * a.nw * 32 * 4;
+    w.hist = reinterpret_cast<uint2 *>(base + off);
+    off += (size_t)entries * a.nw * 32 * 4;          // a.nw = 2 * np words
+    w.lut = reinterpret_cast<uint32_t *>(base + off);
+    if (a.lut) off += (size_t)kLutBuckets * 4;
     w.keys = reinterpret_cast<uint32_t *>(base + off);
     return w;
 }
@@ -204,6 +216,30 @@ __device__ __forceinline__ int find_bin(const uint32_t *keys, int P, uint32_t w)
     int pos = 0;
     for (int step = P >> 1; step > 0; step >>= 1) pos += (keys[pos + step - 1] < w) ? step : 0;
     return pos;
+}
+
+// Bucket table of the segment's keys: bucket b covers the draws with
+// w >> 22 == b.  Entry = (low 22 bits of the bucket's single key, or
+// 0x3FFFFF if it holds none) << 10 | multi-key flag << 9 | bin at the bucket
+// start.  For a bucket with <= 1 key, the bin of any w in it is
+// start + ((w << 10) > entry): one shared load and one compare per request
+// ((w << 10) drops the bucket bits and has zero low bits, so it exceeds the
+// entry iff w's low 22 bits exceed the key's).  Lanes take interleaved
+// buckets (conflict-free stores) and walk the sorted keys with two monotone
+// pointers.
+__device__ __forceinline__ void build_lut(const WarpSmem &W, int K) {
+    const uint32_t lane = lane_id();
+    int c0 = 0, c1 = 0;   // #{keys < b << 22}, #{keys < (b+1) << 22}
+    for (int b = (int)lane; b < kLutBuckets; b += 32) {
+        const uint64_t lo = (uint64_t)b << (32 - kLutBits), hi = (uint64_t)(b + 1) << (32 - kLutBits);
+        while (c0 < K && (uint64_t)W.keys[c0] < lo) ++c0;
+        if (c1 < c0) c1 = c0;
+        while (c1 < K && (uint64_t)W.keys[c1] < hi) ++c1;
+        const int in = c1 - c0;
+        const uint32_t low = in == 1 ? (W.keys[c0] & 0x3FFFFFu) : 0x3FFFFFu;
+        W.lut[b] = (low << 10) | (in >= 2 ? 0x200u : 0u) | (uint32_t)c0;
+    }
+    __syncwarp();
 }
 
 // histogram entry of request k of a group: draw bin, or the class's pinned
@@ -225,74 +261,104 @@ __device__ __forceinline__ int entry_of(int bin, uint2 f, int k, int nb, int NC,
     return inr ? entry : NC * nb;
 }
 
+// move an entry's packed fields into its 64-bit accumulators (rare)
 template <int N>
 __device__ __noinline__ void spill_entry(const WarpSmem &W, int entry, uint32_t lane) {
-    constexpr int NW = Words<N>::NW;
+    constexpr int NP = Words<N>::NP;
+    unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
 #pragma unroll
-    for (int m = 0; m < NW; ++m) {
-        uint32_t *slot = W.hist + ((size_t)entry * NW + m) * 32 + lane;
-        const uint32_t v = *slot;
-        *slot = 0u;
-        atomicAdd(&W.wide[(size_t)entry * (N + 1) + 2 * m], (unsigned long long)(v & 0xFFFFu));
-        if (2 * m + 1 <= N) atomicAdd(&W.wide[(size_t)entry * (N + 1) + 2 * m + 1], (unsigned long long)(v >> 16));
-    }
-}
-
-// A group holding a token >= 2^15 (would overflow the packed fields): add
-// its requests straight into the 64-bit accumulators.
-template <int N, bool FLAGS>
-__device__ __noinline__ void careful_group(const Group<N, FLAGS> &g, const uint32_t (&w)[8], int lo, int hi,
-                                           const SimArgs &a, const WarpSmem &W, int P, uint32_t &err) {
-    for (int k = 0; k < 8; ++k) {
-        const bool inr = k >= lo && k < hi;
-        const int entry = entry_of<FLAGS>(find_bin(W.keys, P, w[k]), g.f, k, a.nb, a.NC, inr, err);
-        if (entry == a.NC * a.nb) continue;
-        unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
-        atomicAdd(&wr[0], 1ull);
+    for (int p = 0; p < NP; ++p) {
+        uint2 *slot = W.hist + ((size_t)entry * NP + p) * 32 + lane;
+        const uint2 v = *slot;
+        *slot = make_uint2(0u, 0u);
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-            uint32_t pw = 0;
-#pragma unroll
-            for (int kk = 0; kk < 8; kk += 2)
-                if ((k >> 1) == (kk >> 1)) pw = plane_word<N, FLAGS>(g, i, kk);
-            atomicAdd(&wr[1 + i], (unsigned long long)half16(pw, k));
+        for (int h = 0; h < 2; ++h) {
+            const int m = 2 * p + h;
+            if (m >= Words<N>::NW) break;
+            const uint32_t x = h ? v.y : v.x;
+            atomicAdd(&wr[word_lo_field(m)], (unsigned long long)(x & 0xFFFFu));
+            if (word_hi_field(m) <= N) atomicAdd(&wr[word_hi_field(m)], (unsigned long long)(x >> 16));
         }
     }
 }
 
+constexpr int kModeSearch = 0;   // level-synchronous binary search over the padded keys
+constexpr int kModeLut = 1;      // bucket table + rare exact search
+
 // One group of 8 requests (local requests 8v..8v+7); requests outside
 // [lo, hi) belong to another segment and go to the discard entry.
-template <int N, bool FLAGS, bool FULL>
+template <int N, bool FLAGS, bool FULL, int MODE>
 __device__ __forceinline__ void process_group(const Group<N, FLAGS> &g, int64_t v, int lo, int hi,
                                               const SimArgs &a, const WarpSmem &W, int P, uint32_t &err) {
     constexpr int NW = Words<N>::NW;
+    constexpr int NP = Words<N>::NP;
     const uint32_t lane = lane_id();
 
     // selection draws of the 8 requests (reading L10): counter (g>>2, 0, 0)
     const uint64_t blk = (a.first_request + (uint64_t)v * 8u) >> 2;
-    const uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
-    const Philox4 d0 = philox4x32_10((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, k0, k1);
-    const Philox4 d1 = philox4x32_10((uint32_t)(blk + 1), (uint32_t)((blk + 1) >> 32), 0u, 0u, k0, k1);
+    const Philox4 d0 = philox4x32_10_rk((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, a.rk0, a.rk1);
+    const Philox4 d1 = philox4x32_10_rk((uint32_t)(blk + 1), (uint32_t)((blk + 1) >> 32), 0u, 0u, a.rk0, a.rk1);
     const uint32_t w[8] = {d0.v[0], d0.v[1], d0.v[2], d0.v[3], d1.v[0], d1.v[1], d1.v[2], d1.v[3]};
+
+    // bins of the 8 draws
+    int bin[8];
+    if (MODE == kModeLut) {
+        uint32_t eor = 0u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t e = W.lut[w[k] >> (32 - kLutBits)];
+            bin[k] = (int)(e & 0x1FFu) + ((w[k] << kLutBits) > e ? 1 : 0);
+            eor |= e;
+        }
+        if (eor & 0x200u) {     // some draw fell in a bucket holding >= 2 keys
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (W.lut[w[k] >> (32 - kLutBits)] & 0x200u) bin[k] = find_bin(W.keys, P, w[k]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) bin[k] = 0;
+        for (int step = P >> 1; step > 0; step >>= 1) {
+            const uint32_t *base = W.keys + (step - 1);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) bin[k] += (base[bin[k]] < w[k]) ? step : 0;
+        }
+    }
 
     uint32_t big = 0u;
 #pragma unroll
     for (int i = 0; i < N; ++i) big |= g.t[i].x | g.t[i].y | g.t[i].z | g.t[i].w;
     if (big & kGuard) {
-        careful_group<N, FLAGS>(g, w, lo, hi, a, W, P, err);
+        // a token >= 2^15 would overflow the packed fields: add this group's
+        // requests straight into the 64-bit accumulators
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const bool inr = FULL || (k >= lo && k < hi);
+            const int entry = entry_of<FLAGS>(bin[k], g.f, k, a.nb, a.NC, inr, err);
+            if (entry != a.NC * a.nb) {
+                unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
+                atomicAdd(&wr[0], 1ull);
+#pragma unroll
+                for (int i = 0; i < N; ++i)
+                    atomicAdd(&wr[1 + i], (unsigned long long)half16(plane_word<N, FLAGS>(g, i, k), k));
+            }
+        }
         return;
     }
+    uint2 *lane_hist = W.hist + lane;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const bool inr = FULL || (k >= lo && k < hi);
-        const int entry = entry_of<FLAGS>(find_bin(W.keys, P, w[k]), g.f, k, a.nb, a.NC, inr, err);
-        uint32_t *slot = W.hist + (size_t)entry * NW * 32 + lane;
+        const int entry = entry_of<FLAGS>(bin[k], g.f, k, a.nb, a.NC, inr, err);
+        uint2 *slot = lane_hist + entry * (NP * 32);
         uint32_t acc = 0u;
 #pragma unroll
-        for (int m = 0; m < NW; ++m) {
-            const uint32_t nv = slot[m * 32] + packed_word<N, FLAGS>(g, m, k);
-            slot[m * 32] = nv;
-            acc |= nv;
+        for (int p = 0; p < NP; ++p) {
+            uint2 cur = slot[p * 32];
+            cur.x += packed_word<N, FLAGS>(g, 2 * p, k) + (p == 0 ? 0x10000u : 0u);
+            if (2 * p + 1 < NW) cur.y += packed_word<N, FLAGS>(g, 2 * p + 1, k);
+            slot[p * 32] = cur;
+            acc |= cur.x | cur.y;
         }
         if (acc & kGuard) spill_entry<N>(W, entry, lane);
     }
@@ -302,7 +368,7 @@ __device__ __forceinline__ void process_group(const Group<N, FLAGS> &g, int64_t 
 // thresholds (count-and-clamp rule) and add into the global per-cell
 // counters with atomics; segment stats go to wide rows [c*nb] / [c*nb+1].
 template <int N, bool FLAGS>
-__device__ __noinline__ void slow_segment(const SimArgs &a, const WarpSmem &W, int64_t sl, int64_t s0, int64_t s1,
+__device__ __forceinline__ void slow_segment(const SimArgs &a, const WarpSmem &W, int64_t sl, int64_t s0, int64_t s1,
                                           uint32_t &err) {
     const uint32_t lane = lane_id();
     const int X = a.X, NC = a.NC;
@@ -357,9 +423,9 @@ __device__ __noinline__ void slow_segment(const SimArgs &a, const WarpSmem &W, i
 // (Eq. 1) and quality.  Fast path: totals = row `tot_row` (prefix total) +
 // the pinned row; slow path: totals in row 0, pinned count in row 1.
 template <int N>
-__device__ __noinline__ void write_seg_stats(const SimArgs &a, const WarpSmem &W, int64_t sl, double kp, double q0,
+__device__ __forceinline__ void write_seg_stats(const SimArgs &a, const WarpSmem &W, int64_t sl, double kp, double q0,
                                              int tot_row, int pin_row, bool fast, const CostConst &cost) {
-    if (lane_id() != 0) return;
+    if (lane_id() == 0) {
     const int NC = a.NC, nb = a.nb;
     double bE = 0.0, bT = 0.0, m = 0.0;
     for (int c = 0; c < NC; ++c) {
@@ -382,6 +448,7 @@ __device__ __noinline__ void write_seg_stats(const SimArgs &a, const WarpSmem &W
     a.seg_base[sl * 4 + 1] = bT;
     a.seg_base[sl * 4 + 2] = kp * bE + a.k1 * bT;
     a.seg_base[sl * 4 + 3] = m * q0;
+    }
 }
 
 __device__ __forceinline__ void zero_cell(const SimArgs &a, int64_t cell, int NCN) {
@@ -392,7 +459,7 @@ __device__ __forceinline__ void zero_cell(const SimArgs &a, int64_t cell, int NC
 // Per-cell integer statistics (from the histogram prefix sums, or from the
 // slow path's global counters) and the closed-form fp64 totals of Eq. 1.
 template <int N>
-__device__ __noinline__ void cell_epilogue(const SimArgs &a, const WarpSmem &W, int64_t sl, int K, double kp,
+__device__ __forceinline__ void cell_epilogue(const SimArgs &a, const WarpSmem &W, int64_t sl, int K, double kp,
                                            const double *qrow, bool fast, const CostConst &cost) {
     const int NC = a.NC, nb = a.nb;
     for (int j = lane_id(); j < a.X; j += 32) {
@@ -442,8 +509,9 @@ __device__ __noinline__ void cell_epilogue(const SimArgs &a, const WarpSmem &W, 
 // Lane-private slots -> 64-bit per-entry totals, then the exclusive prefix
 // over draw bins 0..K+1 per (class, field).
 template <int N>
-__device__ __noinline__ void readout(const SimArgs &a, const WarpSmem &W, int K) {
+__device__ __forceinline__ void readout(const SimArgs &a, const WarpSmem &W, int K) {
     constexpr int NW = Words<N>::NW;
+    constexpr int NP = Words<N>::NP;
     const uint32_t lane = lane_id();
     const int NC = a.NC, nb = a.nb;
     const int used = K + 2;   // draw bins 0..K and the pinned bin
@@ -452,22 +520,29 @@ __device__ __noinline__ void readout(const SimArgs &a, const WarpSmem &W, int K)
         const int entry = c * nb + (b <= K ? b : nb - 1);
         unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
 #pragma unroll
-        for (int m = 0; m < NW; ++m) {
-            uint32_t *row = W.hist + ((size_t)entry * NW + m) * 32;
-            uint32_t slo = 0u, shi = 0u;
+        for (int p = 0; p < NP; ++p) {
+            uint2 *row = W.hist + ((size_t)entry * NP + p) * 32;
+            uint32_t s[4] = {0u, 0u, 0u, 0u};
 #pragma unroll 8
             for (int q = 0; q < 32; ++q) {
                 const int idx = (q + (int)lane) & 31;   // rotated: conflict-free
-                const uint32_t val = row[idx];
-                row[idx] = 0u;
-                slo += val & 0xFFFFu;
-                shi += val >> 16;
+                const uint2 val = row[idx];
+                row[idx] = make_uint2(0u, 0u);
+                s[0] += val.x & 0xFFFFu;
+                s[1] += val.x >> 16;
+                s[2] += val.y & 0xFFFFu;
+                s[3] += val.y >> 16;
             }
-            wr[2 * m] += slo;
-            if (2 * m + 1 <= N) wr[2 * m + 1] += shi;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int m = 2 * p + h;
+                if (m >= NW) break;
+                wr[word_lo_field(m)] += s[2 * h];
+                if (word_hi_field(m) <= N) wr[word_hi_field(m)] += s[2 * h + 1];
+            }
         }
     }
-    for (int i = lane; i < NW * 32; i += 32) W.hist[(size_t)(NC * nb) * NW * 32 + i] = 0u;   // discard entry
+    for (int i = lane; i < NP * 32; i += 32) W.hist[(size_t)(NC * nb) * NP * 32 + i] = make_uint2(0u, 0u);  // discard
     for (int i = lane; i < N + 1; i += 32) W.wide[(size_t)(NC * nb) * (N + 1) + i] = 0ull;
     __syncwarp();
     for (int e = lane; e < NC * (N + 1); e += 32) {
@@ -483,52 +558,79 @@ __device__ __noinline__ void readout(const SimArgs &a, const WarpSmem &W, int K)
     __syncwarp();
 }
 
-template <int N, bool FLAGS>
+// Stream a segment's requests [s0, s1).  Full groups of 8 (all requests in
+// the segment) go through a 3-buffer rotation: lane l takes groups
+// gf + l, gf + l + 32, ...; two groups' loads are in flight while a third is
+// processed, with no register copies between buffers.  Every 128-bit load of
+// the warp covers 512 contiguous bytes of a plane.  The (at most two) partial
+// groups at the segment's ends are handled once, by lanes 0 and 1, in a
+// single convergent call.
+template <int N, bool FLAGS, int MODE>
 __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem &W, int64_t s0, int64_t s1, int P,
                                                uint32_t &err) {
     if (s1 <= s0) return;
-    const int64_t vfirst = s0 >> 3, vlast = (s1 - 1) >> 3;
-    int64_t v = vfirst + lane_id();
-    constexpr int D = N <= 4 ? 2 : 1;   // groups in flight per lane beyond the current pair
-    Group<N, FLAGS> cur[D], nxt[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d)
-        if (v + 32 * d <= vlast) load_group<N, FLAGS>(cur[d], a, v + 32 * d);
-    for (; v <= vlast; v += 32 * D) {
-#pragma unroll
-        for (int d = 0; d < D; ++d)
-            if (v + 32 * (D + d) <= vlast) load_group<N, FLAGS>(nxt[d], a, v + 32 * (D + d));
-#pragma unroll
-        for (int d = 0; d < D; ++d) {
-            const int64_t vv = v + 32 * d;
-            if (vv <= vlast) {
-                const int64_t r0 = vv * 8;
-                const int lo = (int)(s0 > r0 ? s0 - r0 : 0);
-                const int hi = (int)(s1 - r0 < 8 ? s1 - r0 : 8);
-                if (lo == 0 && hi == 8)
-                    process_group<N, FLAGS, true>(cur[d], vv, 0, 8, a, W, P, err);
-                else
-                    process_group<N, FLAGS, false>(cur[d], vv, lo, hi, a, W, P, err);
-            }
+    const uint32_t lane = lane_id();
+    const int64_t gf = (s0 + 7) >> 3;       // first full group
+    const int64_t ge = s1 >> 3;             // one past the last full group
+    {
+        // partial groups: head (s0 not aligned) and tail (s1 not aligned)
+        const int64_t head = s0 >> 3, tail = s1 >> 3;
+        const bool has_head = (s0 & 7) != 0;
+        const bool has_tail = (s1 & 7) != 0 && !(has_head && tail == head);
+        int64_t v = 0;
+        int lo = 0, hi = 0;
+        if (lane == 0 && has_head) {
+            v = head; lo = (int)(s0 & 7); hi = (int)((s1 - (head << 3)) < 8 ? s1 - (head << 3) : 8);
+        } else if (lane == 1 && has_tail) {
+            v = tail; lo = 0; hi = (int)(s1 & 7);
         }
-#pragma unroll
-        for (int d = 0; d < D; ++d) cur[d] = nxt[d];
+        if (__any_sync(0xFFFFFFFFu, hi > lo)) {
+            Group<N, FLAGS> g;
+            if (hi > lo) load_group<N, FLAGS>(g, a, v);
+            else g = Group<N, FLAGS>{};
+            process_group<N, FLAGS, false, MODE>(g, v, lo, hi, a, W, P, err);
+        }
+    }
+    int64_t v = gf + lane;
+    if constexpr (N <= 3) {
+        Group<N, FLAGS> A, B, C;
+        if (v < ge) load_group<N, FLAGS>(A, a, v);
+        if (v + 32 < ge) load_group<N, FLAGS>(B, a, v + 32);
+        for (; v < ge; v += 96) {
+            if (v + 64 < ge) load_group<N, FLAGS>(C, a, v + 64);
+            process_group<N, FLAGS, true, MODE>(A, v, 0, 8, a, W, P, err);
+            if (v + 32 >= ge) break;
+            if (v + 96 < ge) load_group<N, FLAGS>(A, a, v + 96);
+            process_group<N, FLAGS, true, MODE>(B, v + 32, 0, 8, a, W, P, err);
+            if (v + 64 >= ge) break;
+            if (v + 128 < ge) load_group<N, FLAGS>(B, a, v + 128);
+            process_group<N, FLAGS, true, MODE>(C, v + 64, 0, 8, a, W, P, err);
+        }
+    } else {   // wider groups: ping-pong (one group in flight)
+        Group<N, FLAGS> A, B;
+        if (v < ge) load_group<N, FLAGS>(A, a, v);
+        for (; v < ge; v += 64) {
+            if (v + 32 < ge) load_group<N, FLAGS>(B, a, v + 32);
+            process_group<N, FLAGS, true, MODE>(A, v, 0, 8, a, W, P, err);
+            if (v + 32 >= ge) break;
+            if (v + 64 < ge) load_group<N, FLAGS>(A, a, v + 64);
+            process_group<N, FLAGS, true, MODE>(B, v + 32, 0, 8, a, W, P, err);
+        }
     }
 }
 
 template <int N, bool FLAGS>
-__global__ void __launch_bounds__(512, 1) trace_kernel(const __grid_constant__ SimArgs a) {
+__global__ void __launch_bounds__(384, 1) trace_kernel(const __grid_constant__ SimArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ CostConst cost;   // per-launch coefficients (dynamic [class][level] indexing)
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
-    constexpr int NW = Words<N>::NW;
     const WarpSmem W = carve(smem + (size_t)warp * a.warp_smem, a);
     const int NC = a.NC, nb = a.nb, X = a.X;
     const int entries = NC * nb + 1;
     for (int i = threadIdx.x; i < (int)(sizeof(CostConst) / 8); i += blockDim.x)
         reinterpret_cast<double *>(&cost)[i] = reinterpret_cast<const double *>(&a.cost)[i];
-    for (int i = lane; i < entries * NW * 32; i += 32) W.hist[i] = 0u;
+    for (int i = lane; i < entries * Words<N>::NP * 32; i += 32) W.hist[i] = make_uint2(0u, 0u);
     for (int i = lane; i < entries * (N + 1); i += 32) W.wide[i] = 0ull;
     __syncthreads();
 
@@ -570,7 +672,12 @@ __global__ void __launch_bounds__(512, 1) trace_kernel(const __grid_constant__ S
         while (P < K + 1) P <<= 1;
         for (int i = lane; i < P; i += 32) W.keys[i] = i < K ? a.seg_keys[sl * a.kcap + i] : 0xFFFFFFFFu;
         __syncwarp();
-        stream_segment<N, FLAGS>(a, W, s0, s1, P, err);
+        if (a.lut && K >= kLutMinKeys && s1 - s0 >= kLutMinRequests) {
+            build_lut(W, K);
+            stream_segment<N, FLAGS, kModeLut>(a, W, s0, s1, P, err);
+        } else {
+            stream_segment<N, FLAGS, kModeSearch>(a, W, s0, s1, P, err);
+        }
         __syncwarp();
         readout<N>(a, W, K);
         cell_epilogue<N>(a, W, sl, K, kp, qrow, true, cost);
@@ -657,7 +764,7 @@ static int nominal_kcap(int n, int X) {
 bool make_sim_plan(int n, int X, int NC, SimPlan *plan) {
     SimPlan p{};
     p.n = n; p.X = X; p.NC = NC;
-    p.nw = (n + 2) / 2;
+    p.nw = 2 * (((n + 2) / 2 + 1) / 2);   // words allocated per entry: whole 64-bit pairs
     const long M = (long)X * (n - 1);
     int kcap = nominal_kcap(n, X);
     p.sort_cap = 0;
@@ -673,7 +780,9 @@ bool make_sim_plan(int n, int X, int NC, SimPlan *plan) {
         int kp = 1;
         while (kp < kk + 1) kp <<= 1;
         const size_t entries = (size_t)NC * nb + 1;
-        size_t bytes = entries * (n + 1) * 8 + entries * p.nw * 32 * 4 + (size_t)kp * 4;
+        const bool lut = kc >= kLutMinKeys && kc <= kLutMaxKeys;
+        size_t bytes = entries * (n + 1) * 8 + entries * p.nw * 32 * 4 + (size_t)kp * 4 +
+                       (lut ? (size_t)kLutBuckets * 4 : 0);
         *nb_out = nb;
         *kp_out = kp;
         return (bytes + 15) & ~(size_t)15;
@@ -686,11 +795,12 @@ bool make_sim_plan(int n, int X, int NC, SimPlan *plan) {
         bytes = per_warp(kcap, &nb, &kp);
     }
     p.kcap = kcap;
+    p.lut = (kcap >= kLutMinKeys && kcap <= kLutMaxKeys) ? 1 : 0;
     p.nb = nb;
     p.kp = kp;
     p.warp_smem = bytes;
     int wpc = (int)(smem_cap / bytes);
-    if (wpc > 16) wpc = 16;
+    if (wpc > 12) wpc = 12;   // __launch_bounds__(384, 1): up to 168 registers per thread
     if (wpc < 1) return false;
     p.warps_per_cta = wpc;
     *plan = p;
@@ -759,6 +869,14 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
     a.kp = plan.kp;
     a.sort_cap = plan.sort_cap;
     a.warp_smem = plan.warp_smem;
+    a.lut = plan.lut;
+    {
+        uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
+        for (int r = 0; r < 10; ++r) {
+            a.rk0[r] = k0; a.rk1[r] = k1;
+            k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+        }
+    }
 
     // prep (also resets the queue and trace_status)
     {
