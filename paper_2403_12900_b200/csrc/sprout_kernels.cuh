@@ -7,13 +7,13 @@
 
 namespace sprout {
 
-// bin lookup table: 2^10 buckets of the 32-bit draw; an entry holds the bin
-// at the bucket start (9 bits), a multi-key flag and the low 22 bits of the
-// bucket's single breakpoint
+// bin lookup table: 2^10 buckets (64-bit entries) over the range of the keys; an entry holds
+// the bucket's single key and the histogram row offset of the bin at the bucket start
+// (see trace_sim.cu build_lut)
 constexpr int kLutBits = 10;
 constexpr int kLutBuckets = 1 << kLutBits;
 constexpr int kLutMinKeys = 8;      // fewer keys: level-synchronous binary search
-constexpr int kLutMaxKeys = 511;    // bin field width
+constexpr int kLutMaxKeys = 511;    // larger key sets use the binary search
 constexpr int kLutMinRequests = 4096;  // shorter segments do not amortise the table build
 
 struct LpArgs {

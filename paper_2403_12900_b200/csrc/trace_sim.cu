@@ -31,6 +31,9 @@ namespace sprout {
 
 constexpr uint32_t kGuard = 0x80008000u;
 constexpr int kPrepWarps = 4;
+// warps per trace CTA (one CTA per SM): 8 warps = 2 per SM sub-partition leave 255 registers
+// per thread for the 4-deep load rotation and the software pipeline
+constexpr int kMaxTraceWarps = 8;
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
@@ -143,10 +146,16 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(const __grid_cons
 // ---------------------------------------------------------------------------
 // streaming kernel
 //
-// Lane-private histogram entry layout: 16-bit fields packed two per 32-bit
-// word, words grouped in pairs (one 64-bit shared access per pair):
-//   word 0 = tok_0 (low) | count (high);  word m >= 1 = tok_{2m-1} | tok_{2m}.
-// Field f of the 64-bit accumulators ("wide" rows) is 0 = count, 1+i = tok_i.
+// Lane-private histogram entry layout: fields packed two per 32-bit word,
+// words grouped in pairs (one 64-bit shared access per pair):
+//   word 0 = tok_0 (bits 0-19) | count (bits 20-31);
+//   word m >= 1 = tok_{2m-1} (bits 0-15) | tok_{2m} (bits 16-31).
+// The top bit of every field is a guard: a row is spilled into the warp's
+// 64-bit accumulators ("wide" rows; field 0 = count, 1+i = tok_i) once a
+// guard is set, before the next group of 8 requests could overflow it.
+constexpr int kW0Shift = 20;                 // count field of word 0
+constexpr uint32_t kW0Low = (1u << kW0Shift) - 1u;
+constexpr uint32_t kGuard0 = 0x80080000u;    // guards of word 0 (tok_0 >= 2^19, count >= 2^11)
 
 template <int N>
 struct Words {
@@ -193,7 +202,7 @@ __device__ __forceinline__ int word_hi_field(int m) { return m == 0 ? 0 : 2 * m 
 struct WarpSmem {
     uint2 *hist;                 // [(NC*nb + 1)][np][32] lane-private packed pairs
     unsigned long long *wide;    // [(NC*nb + 1)][n+1] 64-bit per-entry totals
-    uint32_t *lut;               // [kLutBuckets] bin lookup table (if a.lut)
+    uint2 *lut;                  // [kLutBuckets] bin lookup table (if a.lut)
     uint32_t *keys;              // [kp] breakpoints - 1, padded with 0xFFFFFFFF
 };
 
@@ -204,10 +213,22 @@ __device__ __forceinline__ WarpSmem carve(uint8_t *base, const SimArgs &a) {
     size_t off = (size_t)entries * (a.n + 1) * 8;
     w.hist = reinterpret_cast<uint2 *>(base + off);
     off += (size_t)entries * a.nw * 32 * 4;          // a.nw = 2 * np words
-    w.lut = reinterpret_cast<uint32_t *>(base + off);
-    if (a.lut) off += (size_t)kLutBuckets * 4;
+    w.lut = reinterpret_cast<uint2 *>(base + off);
+    if (a.lut) off += (size_t)kLutBuckets * 8;
     w.keys = reinterpret_cast<uint32_t *>(base + off);
     return w;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts64(uint32_t addr, uint2 v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(v.x), "r"(v.y) : "memory");
 }
 
 // bin of draw w = #{keys < w}: branchless binary search over P (power of
@@ -218,26 +239,53 @@ __device__ __forceinline__ int find_bin(const uint32_t *keys, int P, uint32_t w)
     return pos;
 }
 
-// Bucket table of the segment's keys: bucket b covers the draws with
-// w >> 22 == b.  Entry = (low 22 bits of the bucket's single key, or
-// 0x3FFFFF if it holds none) << 10 | multi-key flag << 9 | bin at the bucket
-// start.  For a bucket with <= 1 key, the bin of any w in it is
-// start + ((w << 10) > entry): one shared load and one compare per request
-// ((w << 10) drops the bucket bits and has zero low bits, so it exceeds the
-// entry iff w's low 22 bits exceed the key's).  Lanes take interleaved
-// buckets (conflict-free stores) and walk the sorted keys with two monotone
-// pointers.
-__device__ __forceinline__ void build_lut(const WarpSmem &W, int K) {
+// Bucket table of the segment's keys over the draw range [base, 2^32):
+// base = the smallest key rounded down to a multiple of the bucket width 2^s,
+// s the smallest with (2^32 - 1 - base) >> s < kLutBuckets (0 <= s <= 32 - kLutBits).  A
+// draw w is clamped to d = max(w, base) (draws below base are in bin 0) and
+// looked up in bucket (d >> s) - (base >> s).  Entry = {the bucket's single
+// key (0xFFFFFFFF if none), byte offset of the bin at the bucket start in the
+// lane histogram | 4 if the bucket holds >= 2 keys}.  For a bucket with <= 1
+// key the histogram row of d is offset + rowbytes * (d > key): one 64-bit
+// shared load and one compare per request.  Adapting the range to the keys
+// keeps a xi sweep's (uniformly spaced) keys one per bucket even when they
+// crowd near 2^32 (low carbon intensity: mixes close to pure L0).  Lanes take
+// interleaved buckets (conflict-free stores) and walk the sorted keys with
+// two monotone pointers.
+struct LutGeom {
+    uint32_t base;      // aligned range start
+    int s;              // log2 bucket width
+    uint32_t bias;      // shared address of bucket 0 minus (base >> s) * 8
+};
+
+__device__ __forceinline__ LutGeom lut_geometry(const WarpSmem &W, int K) {
+    LutGeom g;
+    const uint32_t kmin = K > 0 ? W.keys[0] : 0u;
+    int s = 0;
+    for (;;) {
+        const uint32_t b = (s >= 32) ? 0u : (kmin & ~((1u << s) - 1u));
+        if (s >= 32 - kLutBits || ((0xFFFFFFFFu - b) >> s) < (uint32_t)kLutBuckets) {
+            g.base = b;
+            break;
+        }
+        ++s;
+    }
+    g.s = s;
+    g.bias = smem_u32(W.lut) - ((g.base >> s) << 3);
+    return g;
+}
+
+__device__ __forceinline__ void build_lut(const WarpSmem &W, int K, LutGeom g, uint32_t rowbytes) {
     const uint32_t lane = lane_id();
-    int c0 = 0, c1 = 0;   // #{keys < b << 22}, #{keys < (b+1) << 22}
+    int c0 = 0, c1 = 0;   // #{keys < lo}, #{keys < hi}
     for (int b = (int)lane; b < kLutBuckets; b += 32) {
-        const uint64_t lo = (uint64_t)b << (32 - kLutBits), hi = (uint64_t)(b + 1) << (32 - kLutBits);
+        const uint64_t lo = (uint64_t)g.base + ((uint64_t)b << g.s);
+        const uint64_t hi = (uint64_t)g.base + ((uint64_t)(b + 1) << g.s);
         while (c0 < K && (uint64_t)W.keys[c0] < lo) ++c0;
         if (c1 < c0) c1 = c0;
         while (c1 < K && (uint64_t)W.keys[c1] < hi) ++c1;
         const int in = c1 - c0;
-        const uint32_t low = in == 1 ? (W.keys[c0] & 0x3FFFFFu) : 0x3FFFFFu;
-        W.lut[b] = (low << 10) | (in >= 2 ? 0x200u : 0u) | (uint32_t)c0;
+        W.lut[b] = make_uint2(in == 1 ? W.keys[c0] : 0xFFFFFFFFu, (uint32_t)c0 * rowbytes | (in >= 2 ? 4u : 0u));
     }
     __syncwarp();
 }
@@ -261,14 +309,23 @@ __device__ __forceinline__ int entry_of(int bin, uint2 f, int k, int nb, int NC,
     return inr ? entry : NC * nb;
 }
 
-// move an entry's packed fields into its 64-bit accumulators (rare)
+// 64-bit accumulator add from several lanes: a native 32-bit shared atomic
+// on the low word, and a carry into the high word when it wraps (rare).
+// (A 64-bit shared atomicAdd would compile to a CAS loop.)
+__device__ __forceinline__ void wide_add(unsigned long long *slot, uint32_t x) {
+    uint32_t *w = reinterpret_cast<uint32_t *>(slot);
+    const uint32_t old = atomicAdd(w, x);
+    if (old + x < old) atomicAdd(w + 1, 1u);
+}
+
+// move a lane's packed row into the warp's 64-bit accumulators (rare)
 template <int N>
-__device__ __noinline__ void spill_entry(const WarpSmem &W, int entry, uint32_t lane) {
+__device__ __forceinline__ void spill_entry(uint2 *hist, unsigned long long *wide, int entry, uint32_t lane) {
     constexpr int NP = Words<N>::NP;
-    unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
+    unsigned long long *wr = wide + (size_t)entry * (N + 1);
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        uint2 *slot = W.hist + ((size_t)entry * NP + p) * 32 + lane;
+        uint2 *slot = hist + ((size_t)entry * NP + p) * 32 + lane;
         const uint2 v = *slot;
         *slot = make_uint2(0u, 0u);
 #pragma unroll
@@ -276,8 +333,8 @@ __device__ __noinline__ void spill_entry(const WarpSmem &W, int entry, uint32_t 
             const int m = 2 * p + h;
             if (m >= Words<N>::NW) break;
             const uint32_t x = h ? v.y : v.x;
-            atomicAdd(&wr[word_lo_field(m)], (unsigned long long)(x & 0xFFFFu));
-            if (word_hi_field(m) <= N) atomicAdd(&wr[word_hi_field(m)], (unsigned long long)(x >> 16));
+            wide_add(&wr[word_lo_field(m)], m == 0 ? (x & kW0Low) : (x & 0xFFFFu));
+            if (word_hi_field(m) <= N) wide_add(&wr[word_hi_field(m)], m == 0 ? (x >> kW0Shift) : (x >> 16));
         }
     }
 }
@@ -285,82 +342,239 @@ __device__ __noinline__ void spill_entry(const WarpSmem &W, int entry, uint32_t 
 constexpr int kModeSearch = 0;   // level-synchronous binary search over the padded keys
 constexpr int kModeLut = 1;      // bucket table + rare exact search
 
-// One group of 8 requests (local requests 8v..8v+7); requests outside
-// [lo, hi) belong to another segment and go to the discard entry.
-template <int N, bool FLAGS, bool FULL, int MODE>
-__device__ __forceinline__ void process_group(const Group<N, FLAGS> &g, int64_t v, int lo, int hi,
-                                              const SimArgs &a, const WarpSmem &W, int P, uint32_t &err) {
-    constexpr int NW = Words<N>::NW;
-    constexpr int NP = Words<N>::NP;
-    const uint32_t lane = lane_id();
+struct U8x {                     // eight per-request words, passed by value
+    uint32_t v[8];
+};
 
-    // selection draws of the 8 requests (reading L10): counter (g>>2, 0, 0)
-    const uint64_t blk = (a.first_request + (uint64_t)v * 8u) >> 2;
+// Selection draws of the 8 requests of group v (local requests 8v..8v+7;
+// reading L10: counter (g>>2, 0, 0), word g&3).
+__device__ __forceinline__ void group_draws_blk(uint64_t blk, const SimArgs &a, U8x &w) {
     const Philox4 d0 = philox4x32_10_rk((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, a.rk0, a.rk1);
     const Philox4 d1 = philox4x32_10_rk((uint32_t)(blk + 1), (uint32_t)((blk + 1) >> 32), 0u, 0u, a.rk0, a.rk1);
-    const uint32_t w[8] = {d0.v[0], d0.v[1], d0.v[2], d0.v[3], d1.v[0], d1.v[1], d1.v[2], d1.v[3]};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) { w.v[k] = d0.v[k]; w.v[4 + k] = d1.v[k]; }
+}
+__device__ __forceinline__ void group_draws(int64_t v, const SimArgs &a, U8x &w) {
+    group_draws_blk((a.first_request + (uint64_t)v * 8u) >> 2, a, w);
+}
 
-    // bins of the 8 draws
-    int bin[8];
+// shared address of the lane's histogram row of one draw, from the bucket
+// table (bit 2 of `eor` flags a multi-key bucket)
+__device__ __forceinline__ uint32_t lut_offset(uint32_t w, LutGeom geo, uint32_t rowbytes, uint32_t lane_base,
+                                               uint32_t &eor) {
+    const uint32_t d = max(w, geo.base);
+    const uint2 e = lds64(geo.bias + ((d >> geo.s) << 3));
+    eor |= e.y;
+    return e.y + lane_base + (d > e.x ? rowbytes : 0u);
+}
+
+// Shared addresses (lane_base + bin * rowbytes) of the histogram rows of the 8 draws.
+// Branch-free: in LUT mode the return value has bit 2 set if some draw fell
+// in a bucket holding >= 2 keys; the caller repairs those with fix_offsets().
+template <int MODE>
+__device__ __forceinline__ uint32_t group_offsets(const U8x &w, const WarpSmem &W, int P, LutGeom geo,
+                                                  uint32_t rowbytes, uint32_t lane_base, U8x &off) {
+    uint32_t eor = 0u;
     if (MODE == kModeLut) {
-        uint32_t eor = 0u;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t e = W.lut[w[k] >> (32 - kLutBits)];
-            bin[k] = (int)(e & 0x1FFu) + ((w[k] << kLutBits) > e ? 1 : 0);
-            eor |= e;
-        }
-        if (eor & 0x200u) {     // some draw fell in a bucket holding >= 2 keys
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-                if (W.lut[w[k] >> (32 - kLutBits)] & 0x200u) bin[k] = find_bin(W.keys, P, w[k]);
-        }
+        for (int k = 0; k < 8; ++k) off.v[k] = lut_offset(w.v[k], geo, rowbytes, lane_base, eor);
     } else {
+        int bin[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) bin[k] = 0;
         for (int step = P >> 1; step > 0; step >>= 1) {
             const uint32_t *base = W.keys + (step - 1);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) bin[k] += (base[bin[k]] < w[k]) ? step : 0;
+            for (int k = 0; k < 8; ++k) bin[k] += (base[bin[k]] < w.v[k]) ? step : 0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) off.v[k] = lane_base + (uint32_t)bin[k] * rowbytes;
+    }
+    return eor;
+}
+
+// exact offsets for the draws that fell in multi-key buckets (rare; inline:
+// a call would make the warp wait for its in-flight prefetch loads)
+__device__ __forceinline__ void fix_offsets(const U8x &w, U8x &off, const uint32_t *keys, int P, LutGeom geo,
+                                            uint32_t rowbytes, uint32_t lane_base) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t d = max(w.v[k], geo.base);
+        if (lds64(geo.bias + ((d >> geo.s) << 3)).y & 4u) {
+            int pos = 0;
+#pragma unroll 1
+            for (int step = P >> 1; step > 0; step >>= 1) pos += (keys[pos + step - 1] < w.v[k]) ? step : 0;
+            off.v[k] = lane_base + (uint32_t)pos * rowbytes;
         }
     }
+}
 
+// row byte offset of request k: the draw's bin, or (FLAGS) the class's pinned
+// bin, offset by class; the discard row for bad classes
+template <bool FLAGS>
+__device__ __forceinline__ uint32_t row_of(uint32_t off, uint2 f, int k, uint32_t pin_off, uint32_t class_bytes,
+                                           int NC, uint32_t discard_off, uint32_t &err) {
+    if (!FLAGS) return off;
+    const uint32_t fw = (k < 4) ? f.x : f.y;
+    const uint32_t fb = (fw >> (8 * (k & 3))) & 0xFFu;
+    const uint32_t cls = (fb >> 1) & 3u;
+    uint32_t r = ((fb & 1u) ? pin_off : off) + cls * class_bytes;
+    if (cls >= (uint32_t)NC) {
+        r = discard_off;
+        err |= SPROUT_TRACE_BAD_CLASS;
+    }
+    return r;
+}
+
+// add one request straight into the 64-bit accumulators of its entry
+template <int N, bool FLAGS>
+__device__ __forceinline__ void add_wide(unsigned long long *wide, const Group<N, FLAGS> &g, int entry, int k) {
+    unsigned long long *wr = wide + (size_t)entry * (N + 1);
+    wide_add(&wr[0], 1u);
+#pragma unroll
+    for (int i = 0; i < N; ++i) wide_add(&wr[1 + i], half16(plane_word<N, FLAGS>(g, i, k), k));
+}
+
+// packed increment of word m >= 1 of request k: tok_{2m-1} | tok_{2m} << 16
+template <int N, bool FLAGS>
+__device__ __forceinline__ uint32_t packed_hi(const Group<N, FLAGS> &g, int m, int k) {
+    const uint32_t lo_src = plane_word<N, FLAGS>(g, 2 * m - 1, k);
+    const uint32_t hi_src = (2 * m <= N - 1) ? plane_word<N, FLAGS>(g, 2 * m, k) : 0u;
+    return __byte_perm(lo_src, hi_src, (k & 1) ? 0x7632u : 0x5410u);
+}
+
+// OR of every token word of the group (bits 12-15 of a field set <=> a token >= 4096)
+template <int N, bool FLAGS>
+__device__ __forceinline__ uint32_t group_or(const Group<N, FLAGS> &g) {
     uint32_t big = 0u;
 #pragma unroll
     for (int i = 0; i < N; ++i) big |= g.t[i].x | g.t[i].y | g.t[i].z | g.t[i].w;
-    if (big & kGuard) {
-        // a token >= 2^15 would overflow the packed fields: add this group's
-        // requests straight into the 64-bit accumulators
+    return big;
+}
+constexpr uint32_t kBigTok = 0xF000F000u;
+
+// Fast update of a full group: for each request, one 64-bit shared load,
+// packed adds (word 0 += tok_0 + 1<<16, the count; word m += tok_{2m-1} |
+// tok_{2m} << 16) and a store per word pair of its lane-private row, with no
+// branch (one basic block, so the scheduler can interleave it with the next
+// group's Philox rounds).  Every field is below its guard bit before the
+// group (guard invariant: 2^15 for 16-bit token fields, 2^19 for tok_0, 2^11
+// for the count) and gains at most 8 * 4095 (tokens < 4096) or 8 (count), so
+// no field can overflow inside the group; the caller checks the returned
+// guard bits of the stored words afterwards, and redoes the group through
+// the 64-bit path if it had a token >= 4096.  Stores happen in request
+// order, so two requests of the group hitting the same row are serialised
+// through shared memory correctly.
+template <int N, bool FLAGS>
+__device__ __forceinline__ void rmw_row(const Group<N, FLAGS> &g, int k, uint32_t addr, uint32_t &acc0,
+                                        uint32_t &acc) {
+    constexpr int NW = Words<N>::NW;
+    constexpr int NP = Words<N>::NP;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        uint2 cur = lds64(addr + p * 256);
+        if (p == 0) {
+            const uint32_t w0 = plane_word<N, FLAGS>(g, 0, k);
+            cur.x += ((k & 1) ? (w0 >> 16) : (w0 & 0xFFFFu)) + (1u << kW0Shift);
+        } else {
+            cur.x += packed_hi<N, FLAGS>(g, 2 * p, k);
+        }
+        if (2 * p + 1 < NW) cur.y += packed_hi<N, FLAGS>(g, 2 * p + 1, k);
+        sts64(addr + p * 256, cur);
+        if (p == 0) { acc0 |= cur.x; acc |= cur.y; } else { acc |= cur.x | cur.y; }
+    }
+}
+
+// The read-modify-write chain of a group (request k's load may alias
+// request k-1's store, so the 8 updates are serialised through shared
+// memory) interleaved, in program order, with the bucket-table lookups of
+// the lane's next group: each lookup issues right behind a store and its
+// result is only needed in the next iteration, so it fills the chain's
+// load-latency gaps instead of running before it.  Returns the guard bits.
+template <int N, bool FLAGS, int MODE>
+__device__ __forceinline__ uint32_t update_fast(const Group<N, FLAGS> &g, const U8x &row, uint32_t lane_base,
+                                                const U8x &wn, const WarpSmem &W, int P, LutGeom geo,
+                                                uint32_t rowbytes, U8x &on, uint32_t &en) {
+    uint32_t acc0 = 0u, acc = 0u;
+    if (MODE == kModeLut) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            const bool inr = FULL || (k >= lo && k < hi);
-            const int entry = entry_of<FLAGS>(bin[k], g.f, k, a.nb, a.NC, inr, err);
-            if (entry != a.NC * a.nb) {
-                unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
-                atomicAdd(&wr[0], 1ull);
-#pragma unroll
-                for (int i = 0; i < N; ++i)
-                    atomicAdd(&wr[1 + i], (unsigned long long)half16(plane_word<N, FLAGS>(g, i, k), k));
-            }
+            rmw_row<N, FLAGS>(g, k, row.v[k], acc0, acc);
+            on.v[k] = lut_offset(wn.v[k], geo, rowbytes, lane_base, en);
         }
-        return;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) rmw_row<N, FLAGS>(g, k, row.v[k], acc0, acc);
+        en = group_offsets<MODE>(wn, W, P, geo, rowbytes, lane_base, on);
     }
-    uint2 *lane_hist = W.hist + lane;
+    return (acc0 & kGuard0) | (acc & kGuard);
+}
+
+// Rare paths, inline (a call would make the warp wait for its in-flight
+// prefetch loads): revert a fast update (exact: 32-bit word arithmetic is modular) and add the
+// group's requests into the 64-bit accumulators instead ...
+template <int N, bool FLAGS>
+__device__ __forceinline__ void redo_wide(const Group<N, FLAGS> &g, const U8x &row, uint32_t lane_base,
+                                          unsigned long long *wide,
+                                       uint32_t rowbytes, uint32_t discard_off) {
+    constexpr int NW = Words<N>::NW;
+    constexpr int NP = Words<N>::NP;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        const bool inr = FULL || (k >= lo && k < hi);
-        const int entry = entry_of<FLAGS>(bin[k], g.f, k, a.nb, a.NC, inr, err);
-        uint2 *slot = lane_hist + entry * (NP * 32);
+        const uint32_t addr = row.v[k];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+            uint2 cur = lds64(addr + p * 256);
+            if (p == 0) {
+                const uint32_t w0 = plane_word<N, FLAGS>(g, 0, k);
+                cur.x -= ((k & 1) ? (w0 >> 16) : (w0 & 0xFFFFu)) + (1u << kW0Shift);
+            } else {
+                cur.x -= packed_hi<N, FLAGS>(g, 2 * p, k);
+            }
+            if (2 * p + 1 < NW) cur.y -= packed_hi<N, FLAGS>(g, 2 * p + 1, k);
+            sts64(addr + p * 256, cur);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (row.v[k] != lane_base + discard_off)
+            add_wide<N, FLAGS>(wide, g, (int)((row.v[k] - lane_base) / rowbytes), k);
+}
+
+// ... and spill every row of the group with a guard bit set
+template <int N>
+__device__ __forceinline__ void spill_group(const U8x &row, uint2 *hist, unsigned long long *wide, uint32_t lane,
+                                            uint32_t rowbytes, uint32_t lane_base) {
+    constexpr int NP = Words<N>::NP;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int entry = (int)((row.v[k] - lane_base) / rowbytes);
         uint32_t acc = 0u;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            uint2 cur = slot[p * 32];
-            cur.x += packed_word<N, FLAGS>(g, 2 * p, k) + (p == 0 ? 0x10000u : 0u);
-            if (2 * p + 1 < NW) cur.y += packed_word<N, FLAGS>(g, 2 * p + 1, k);
-            slot[p * 32] = cur;
-            acc |= cur.x | cur.y;
+            const uint2 v = hist[((size_t)entry * NP + p) * 32 + lane];
+            acc |= (p == 0 ? (v.x & kGuard0) : (v.x & kGuard)) | (v.y & kGuard);
         }
-        if (acc & kGuard) spill_entry<N>(W, entry, lane);
+        if (acc) spill_entry<N>(hist, wide, entry, lane);
+    }
+}
+
+// One partial group (requests outside [lo, hi) belong to another segment) --
+// the careful 64-bit path, used at segment ends.
+template <int N, bool FLAGS, int MODE>
+__device__ __forceinline__ void process_partial(const Group<N, FLAGS> &g, int64_t v, int lo, int hi,
+                                                const SimArgs &a, const WarpSmem &W, int P, LutGeom geo,
+                                                uint32_t &err) {
+    const uint32_t rowbytes = Words<N>::NP * 256;
+    U8x w, off;
+    group_draws(v, a, w);
+    const uint32_t eor = group_offsets<MODE>(w, W, P, geo, rowbytes, 0u, off);
+    if (MODE == kModeLut && (eor & 4u)) fix_offsets(w, off, W.keys, P, geo, rowbytes, 0u);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const bool inr = k >= lo && k < hi;
+        const int entry = entry_of<FLAGS>((int)(off.v[k] / rowbytes), g.f, k, a.nb, a.NC, inr, err);
+        if (entry != a.NC * a.nb) add_wide<N, FLAGS>(W.wide, g, entry, k);
     }
 }
 
@@ -528,8 +742,8 @@ __device__ __forceinline__ void readout(const SimArgs &a, const WarpSmem &W, int
                 const int idx = (q + (int)lane) & 31;   // rotated: conflict-free
                 const uint2 val = row[idx];
                 row[idx] = make_uint2(0u, 0u);
-                s[0] += val.x & 0xFFFFu;
-                s[1] += val.x >> 16;
+                s[0] += p == 0 ? (val.x & kW0Low) : (val.x & 0xFFFFu);
+                s[1] += p == 0 ? (val.x >> kW0Shift) : (val.x >> 16);
                 s[2] += val.y & 0xFFFFu;
                 s[3] += val.y >> 16;
             }
@@ -558,22 +772,42 @@ __device__ __forceinline__ void readout(const SimArgs &a, const WarpSmem &W, int
     __syncwarp();
 }
 
-// Stream a segment's requests [s0, s1).  Full groups of 8 (all requests in
-// the segment) go through a 3-buffer rotation: lane l takes groups
-// gf + l, gf + l + 32, ...; two groups' loads are in flight while a third is
-// processed, with no register copies between buffers.  Every 128-bit load of
-// the warp covers 512 contiguous bytes of a plane.  The (at most two) partial
-// groups at the segment's ends are handled once, by lanes 0 and 1, in a
-// single convergent call.
+// L2 prefetch distance of the streaming loop, in warp iterations (one
+// iteration = 32 groups = 512 contiguous bytes per token plane)
+constexpr int kPrefetchIters = 8;
+
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Stream a segment's requests [s0, s1).  Lane l takes the full groups
+// gf + l, gf + l + 32, ... (warp iteration i covers groups gf + 32i ..
+// gf + 32i + 31: every 128-bit load of the warp reads 512 contiguous bytes
+// of a plane).  Memory-level parallelism comes from L2 prefetches of the
+// lane's group kPrefetchIters iterations ahead (one per plane, no
+// registers held), so the register loads -- one group ahead, ping-pong --
+// hit L2; this keeps the unrolled loop to two bodies (instruction-cache
+// footprint).  Software pipeline: while
+// group v's tokens are added into the histogram, the Philox draws and
+// histogram rows of the lane's next group v+32 are computed in the same
+// basic block (they do not depend on token data), so the scheduler overlaps
+// the integer rounds with the shared-memory read-modify-write chain.  The
+// (at most two) partial groups at the segment's ends take the careful
+// 64-bit path.
 template <int N, bool FLAGS, int MODE>
 __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem &W, int64_t s0, int64_t s1, int P,
-                                               uint32_t &err) {
+                                               LutGeom geo, uint32_t &err) {
     if (s1 <= s0) return;
     const uint32_t lane = lane_id();
     const int64_t gf = (s0 + 7) >> 3;       // first full group
     const int64_t ge = s1 >> 3;             // one past the last full group
+    auto prefetch_group = [&](int64_t v) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) prefetch_l2(reinterpret_cast<const uint4 *>(a.tokens + (size_t)i * a.pitch) + v);
+    };
+    for (int it = 1; it < kPrefetchIters; ++it)
+        if (gf + lane + 32 * it < ge) prefetch_group(gf + lane + 32 * it);
     {
-        // partial groups: head (s0 not aligned) and tail (s1 not aligned)
         const int64_t head = s0 >> 3, tail = s1 >> 3;
         const bool has_head = (s0 & 7) != 0;
         const bool has_tail = (s1 & 7) != 0 && !(has_head && tail == head);
@@ -584,43 +818,85 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
         } else if (lane == 1 && has_tail) {
             v = tail; lo = 0; hi = (int)(s1 & 7);
         }
-        if (__any_sync(0xFFFFFFFFu, hi > lo)) {
+        if (hi > lo) {
             Group<N, FLAGS> g;
-            if (hi > lo) load_group<N, FLAGS>(g, a, v);
-            else g = Group<N, FLAGS>{};
-            process_group<N, FLAGS, false, MODE>(g, v, lo, hi, a, W, P, err);
+            load_group<N, FLAGS>(g, a, v);
+            process_partial<N, FLAGS, MODE>(g, v, lo, hi, a, W, P, geo, err);
         }
     }
-    int64_t v = gf + lane;
-    if constexpr (N <= 3) {
-        Group<N, FLAGS> A, B, C;
-        if (v < ge) load_group<N, FLAGS>(A, a, v);
-        if (v + 32 < ge) load_group<N, FLAGS>(B, a, v + 32);
-        for (; v < ge; v += 96) {
-            if (v + 64 < ge) load_group<N, FLAGS>(C, a, v + 64);
-            process_group<N, FLAGS, true, MODE>(A, v, 0, 8, a, W, P, err);
-            if (v + 32 >= ge) break;
-            if (v + 96 < ge) load_group<N, FLAGS>(A, a, v + 96);
-            process_group<N, FLAGS, true, MODE>(B, v + 32, 0, 8, a, W, P, err);
-            if (v + 64 >= ge) break;
-            if (v + 128 < ge) load_group<N, FLAGS>(B, a, v + 128);
-            process_group<N, FLAGS, true, MODE>(C, v + 64, 0, 8, a, W, P, err);
-        }
-    } else {   // wider groups: ping-pong (one group in flight)
-        Group<N, FLAGS> A, B;
-        if (v < ge) load_group<N, FLAGS>(A, a, v);
-        for (; v < ge; v += 64) {
-            if (v + 32 < ge) load_group<N, FLAGS>(B, a, v + 32);
-            process_group<N, FLAGS, true, MODE>(A, v, 0, 8, a, W, P, err);
-            if (v + 32 >= ge) break;
-            if (v + 64 < ge) load_group<N, FLAGS>(A, a, v + 64);
-            process_group<N, FLAGS, true, MODE>(B, v + 32, 0, 8, a, W, P, err);
+    constexpr uint32_t rowbytes = Words<N>::NP * 256;
+    const uint32_t lane_base = smem_u32(W.hist) + lane * 8u;
+    const uint32_t discard_row = lane_base + (uint32_t)(a.NC * a.nb) * rowbytes;
+    const uint32_t pin_row = lane_base + (uint32_t)(a.nb - 1) * rowbytes;
+    const uint32_t class_bytes = (uint32_t)a.nb * rowbytes;
+    const int64_t v0 = gf + lane;
+    const uint32_t n_mine = v0 < ge ? (uint32_t)((ge - v0 + 31) >> 5) : 0u;   // this lane's groups
+    if (n_mine == 0) return;
+    // Per-lane cursors advanced by one warp iteration (32 groups) per body:
+    // token plane 0 at the lane's current group (planes i > 0 at + i * pitch),
+    // flags, and the Philox block of the group two iterations ahead.
+    const uint8_t *tp = reinterpret_cast<const uint8_t *>(a.tokens) + (size_t)v0 * 16u;
+    const size_t pb = (size_t)a.pitch * 2u;
+    const uint8_t *fp = FLAGS ? a.flags + (size_t)v0 * 8u : nullptr;
+    uint64_t blk = ((a.first_request + (uint64_t)v0 * 8u) >> 2) + 128u;
+    auto load_at = [&](Group<N, FLAGS> &g, int it) {   // group of iteration (current + it)
+#pragma unroll
+        for (int i = 0; i < N; ++i) g.t[i] = __ldcs(reinterpret_cast<const uint4 *>(tp + i * pb) + 32 * it);
+        if (FLAGS) g.f = __ldcs(reinterpret_cast<const uint2 *>(fp) + 32 * it);
+    };
+
+    // Pipeline state (ping-pong names, so no register copies): body b works
+    // on group v with rows oc[b]; it looks up the rows of v+32 (into
+    // oc[b^1]) from the draws wq[b] computed one body earlier, and draws
+    // for v+64 (into wq[b^1]).  The three chains -- Philox rounds, table
+    // lookups, histogram read-modify-writes -- are mutually independent
+    // inside a body.  All rare work (a token >= 4096, a guard bit, a
+    // multi-key bucket) sits behind one branch per body.
+    Group<N, FLAGS> g[2];
+    U8x oc[2], wq[2];
+    load_at(g[0], 0);
+    {
+        U8x w;
+        group_draws_blk(blk - 128u, a, w);
+        const uint32_t e = group_offsets<MODE>(w, W, P, geo, rowbytes, lane_base, oc[0]);
+        if (MODE == kModeLut && (e & 4u)) fix_offsets(w, oc[0], W.keys, P, geo, rowbytes, lane_base);
+        group_draws_blk(blk - 64u, a, wq[0]);
+    }
+    for (uint32_t i0 = 0; i0 < n_mine; i0 += 2) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            const uint32_t i = i0 + b;
+            if (i < n_mine) {
+                if (i + kPrefetchIters < n_mine)
+#pragma unroll
+                    for (int q = 0; q < N; ++q)
+                        prefetch_l2(reinterpret_cast<const uint4 *>(tp + q * pb) + 32 * kPrefetchIters);
+                if (i + 1 < n_mine) load_at(g[b ^ 1], 1);
+                group_draws_blk(blk, a, wq[b ^ 1]);
+                U8x row;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    row.v[k] = row_of<FLAGS>(oc[b].v[k], g[b].f, k, pin_row, class_bytes, a.NC, discard_row, err);
+                uint32_t en = 0u;
+                const uint32_t acc =
+                    update_fast<N, FLAGS, MODE>(g[b], row, lane_base, wq[b], W, P, geo, rowbytes, oc[b ^ 1], en);
+                const uint32_t big = group_or<N, FLAGS>(g[b]) & kBigTok;
+                if (big | acc | (MODE == kModeLut ? (en & 4u) : 0u)) {
+                    if (big) redo_wide<N, FLAGS>(g[b], row, lane_base, W.wide, rowbytes, discard_row - lane_base);
+                    if (acc) spill_group<N>(row, W.hist, W.wide, lane, rowbytes, lane_base);
+                    if (MODE == kModeLut && (en & 4u))
+                        fix_offsets(wq[b], oc[b ^ 1], W.keys, P, geo, rowbytes, lane_base);
+                }
+                tp += 512;
+                if (FLAGS) fp += 256;
+                blk += 64u;
+            }
         }
     }
 }
 
 template <int N, bool FLAGS>
-__global__ void __launch_bounds__(384, 1) trace_kernel(const __grid_constant__ SimArgs a) {
+__global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __grid_constant__ SimArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ CostConst cost;   // per-launch coefficients (dynamic [class][level] indexing)
     const int warp = threadIdx.x >> 5;
@@ -673,10 +949,11 @@ __global__ void __launch_bounds__(384, 1) trace_kernel(const __grid_constant__ S
         for (int i = lane; i < P; i += 32) W.keys[i] = i < K ? a.seg_keys[sl * a.kcap + i] : 0xFFFFFFFFu;
         __syncwarp();
         if (a.lut && K >= kLutMinKeys && s1 - s0 >= kLutMinRequests) {
-            build_lut(W, K);
-            stream_segment<N, FLAGS, kModeLut>(a, W, s0, s1, P, err);
+            const LutGeom geo = lut_geometry(W, K);
+            build_lut(W, K, geo, Words<N>::NP * 256);
+            stream_segment<N, FLAGS, kModeLut>(a, W, s0, s1, P, geo, err);
         } else {
-            stream_segment<N, FLAGS, kModeSearch>(a, W, s0, s1, P, err);
+            stream_segment<N, FLAGS, kModeSearch>(a, W, s0, s1, P, LutGeom{0u, 32 - kLutBits, 0u}, err);
         }
         __syncwarp();
         readout<N>(a, W, K);
@@ -782,7 +1059,7 @@ bool make_sim_plan(int n, int X, int NC, SimPlan *plan) {
         const size_t entries = (size_t)NC * nb + 1;
         const bool lut = kc >= kLutMinKeys && kc <= kLutMaxKeys;
         size_t bytes = entries * (n + 1) * 8 + entries * p.nw * 32 * 4 + (size_t)kp * 4 +
-                       (lut ? (size_t)kLutBuckets * 4 : 0);
+                       (lut ? (size_t)kLutBuckets * 8 : 0);
         *nb_out = nb;
         *kp_out = kp;
         return (bytes + 15) & ~(size_t)15;
@@ -800,7 +1077,7 @@ bool make_sim_plan(int n, int X, int NC, SimPlan *plan) {
     p.kp = kp;
     p.warp_smem = bytes;
     int wpc = (int)(smem_cap / bytes);
-    if (wpc > 12) wpc = 12;   // __launch_bounds__(384, 1): up to 168 registers per thread
+    if (wpc > kMaxTraceWarps) wpc = kMaxTraceWarps;
     if (wpc < 1) return false;
     p.warps_per_cta = wpc;
     *plan = p;
