@@ -41,12 +41,49 @@ __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 // prep: one warp per segment.  Validates the segment's offsets, merges the
 // nonzero thresholds of its valid cells into sorted distinct keys, and for
 // each valid cell the first bin of levels 1..n-1 (count-and-clamp rule).
+// E > 0: the (<= 32E) thresholds are sorted in registers, E per lane, by a
+// warp bitonic network (shuffles across lanes, register swaps within); E = 0:
+// generic shared-memory bitonic sort for larger sets.
+
+// bitonic sort, ascending, of 32E values held E per lane (element i = lane*E + e)
+template <int E>
+__device__ __forceinline__ void warp_bitonic_sort(uint32_t (&v)[E], uint32_t lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= E) {
+                const int lj = j / E;
+                const bool lower = (lane & (uint32_t)lj) == 0u;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, v[e], lj);
+                    const bool up = (((int)lane * E + e) & k) == 0;
+                    v[e] = (lower == up) ? min(v[e], other) : max(v[e], other);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if ((e & j) == 0) {
+                        const bool up = (((int)lane * E + e) & k) == 0;
+                        const uint32_t lo = min(v[e], v[e ^ j]), hi = max(v[e], v[e ^ j]);
+                        v[e] = up ? lo : hi;
+                        v[e ^ j] = up ? hi : lo;
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int E>
 __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(const __grid_constant__ SimArgs a) {
     extern __shared__ uint32_t prep_smem[];
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
-    uint32_t *buf = prep_smem + (size_t)warp * 2 * (a.sort_cap > 0 ? a.sort_cap : 1);
-    uint32_t *keys = buf + (a.sort_cap > 0 ? a.sort_cap : 1);
+    const int scap = E > 0 ? 32 * E : (a.sort_cap > 0 ? a.sort_cap : 1);
+    uint32_t *buf = prep_smem + (size_t)warp * 2 * scap;
+    uint32_t *keys = buf + scap;
     const int n = a.n, X = a.X;
     const int nt = n - 1;
 
@@ -67,41 +104,75 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(const __grid_cons
             continue;
         }
         const int M = X * nt;
-        const int cap = a.sort_cap;
-        // gather nonzero thresholds of valid cells (0 = empty slot)
-        for (int idx = lane; idx < cap; idx += 32) {
-            uint32_t v = 0u;
-            if (idx < M) {
-                const int64_t cell = sl * X + idx / nt;
-                if (a.cell_status[cell] == SPROUT_CELL_OK) v = a.threshold[cell * nt + idx % nt];
-            }
-            buf[idx] = v;
-        }
-        __syncwarp();
-        // bitonic sort ascending
-        for (int k = 2; k <= cap; k <<= 1) {
-            for (int jj = k >> 1; jj > 0; jj >>= 1) {
-                for (int i = lane; i < cap; i += 32) {
-                    const int ixj = i ^ jj;
-                    if (ixj > i) {
-                        const uint32_t u = buf[i], v = buf[ixj];
-                        const bool up = (i & k) == 0;
-                        if ((u > v) == up) { buf[i] = v; buf[ixj] = u; }
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        // compact distinct nonzero keys
         int K = 0;
-        for (int base = 0; base < cap; base += 32) {
-            const int i = base + lane;
-            const uint32_t v = buf[i];
-            const bool first = v != 0u && (i == 0 || buf[i - 1] != v);
-            const uint32_t bal = __ballot_sync(0xFFFFFFFFu, first);
-            const int rank = K + __popc(bal & ((1u << lane) - 1u));
-            if (first) keys[rank] = v;
-            K += __popc(bal);
+        if constexpr (E > 0) {
+            // gather nonzero thresholds of valid cells (0 = empty slot)
+            uint32_t v[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int idx = (int)lane * E + e;
+                v[e] = 0u;
+                if (idx < M) {
+                    const int64_t cell = sl * X + idx / nt;
+                    if (a.cell_status[cell] == SPROUT_CELL_OK) v[e] = a.threshold[cell * nt + idx % nt];
+                }
+            }
+            warp_bitonic_sort<E>(v, lane);
+            // compact distinct nonzero keys: rank = exclusive count of first occurrences
+            const uint32_t prev_last = __shfl_up_sync(0xFFFFFFFFu, v[E - 1], 1);
+            uint32_t firsts = 0u;
+            int cnt = 0;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const uint32_t prev = e > 0 ? v[e - 1] : (lane > 0 ? prev_last : 0u);
+                const bool first = v[e] != 0u && v[e] != prev;
+                firsts |= first ? (1u << e) : 0u;
+                cnt += first ? 1 : 0;
+            }
+            int incl = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+                if ((int)lane >= d) incl += y;
+            }
+            K = __shfl_sync(0xFFFFFFFFu, incl, 31);
+            int r = incl - cnt;
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                if (firsts & (1u << e)) keys[r++] = v[e];
+        } else {
+            const int cap = a.sort_cap;
+            for (int idx = lane; idx < cap; idx += 32) {
+                uint32_t v = 0u;
+                if (idx < M) {
+                    const int64_t cell = sl * X + idx / nt;
+                    if (a.cell_status[cell] == SPROUT_CELL_OK) v = a.threshold[cell * nt + idx % nt];
+                }
+                buf[idx] = v;
+            }
+            __syncwarp();
+            for (int k = 2; k <= cap; k <<= 1) {
+                for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                    for (int i = lane; i < cap; i += 32) {
+                        const int ixj = i ^ jj;
+                        if (ixj > i) {
+                            const uint32_t u = buf[i], v = buf[ixj];
+                            const bool up = (i & k) == 0;
+                            if ((u > v) == up) { buf[i] = v; buf[ixj] = u; }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            for (int base = 0; base < cap; base += 32) {
+                const int i = base + lane;
+                const uint32_t v = buf[i];
+                const bool first = v != 0u && (i == 0 || buf[i - 1] != v);
+                const uint32_t bal = __ballot_sync(0xFFFFFFFFu, first);
+                const int rank = K + __popc(bal & ((1u << lane) - 1u));
+                if (first) keys[rank] = v;
+                K += __popc(bal);
+            }
         }
         __syncwarp();
         if (K > a.kcap) {
@@ -139,6 +210,7 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(const __grid_cons
                 a.seg_bnd[cell * nt + (L - 1)] = (uint16_t)bnd;
             }
         }
+        __syncwarp();
         if (lane == 0) a.seg_meta[sl] = K;
     }
 }
@@ -249,9 +321,7 @@ __device__ __forceinline__ int find_bin(const uint32_t *keys, int P, uint32_t w)
 // key the histogram row of d is offset + rowbytes * (d > key): one 64-bit
 // shared load and one compare per request.  Adapting the range to the keys
 // keeps a xi sweep's (uniformly spaced) keys one per bucket even when they
-// crowd near 2^32 (low carbon intensity: mixes close to pure L0).  Lanes take
-// interleaved buckets (conflict-free stores) and walk the sorted keys with
-// two monotone pointers.
+// crowd near 2^32 (low carbon intensity: mixes close to pure L0).
 struct LutGeom {
     uint32_t base;      // aligned range start
     int s;              // log2 bucket width
@@ -275,17 +345,45 @@ __device__ __forceinline__ LutGeom lut_geometry(const WarpSmem &W, int K) {
     return g;
 }
 
+// Build: clear the table, scatter the keys (count in .y, key in .x), then an
+// exclusive prefix over the bucket counts, 32 buckets per step (lane = bucket
+// within the chunk; two ballots of the counts' low bits give the in-chunk
+// prefix unless some count is >= 4, then a shuffle scan).
 __device__ __forceinline__ void build_lut(const WarpSmem &W, int K, LutGeom g, uint32_t rowbytes) {
     const uint32_t lane = lane_id();
-    int c0 = 0, c1 = 0;   // #{keys < lo}, #{keys < hi}
-    for (int b = (int)lane; b < kLutBuckets; b += 32) {
-        const uint64_t lo = (uint64_t)g.base + ((uint64_t)b << g.s);
-        const uint64_t hi = (uint64_t)g.base + ((uint64_t)(b + 1) << g.s);
-        while (c0 < K && (uint64_t)W.keys[c0] < lo) ++c0;
-        if (c1 < c0) c1 = c0;
-        while (c1 < K && (uint64_t)W.keys[c1] < hi) ++c1;
-        const int in = c1 - c0;
-        W.lut[b] = make_uint2(in == 1 ? W.keys[c0] : 0xFFFFFFFFu, (uint32_t)c0 * rowbytes | (in >= 2 ? 4u : 0u));
+    for (int b = (int)lane; b < kLutBuckets; b += 32) W.lut[b] = make_uint2(0xFFFFFFFFu, 0u);
+    __syncwarp();
+    for (int j = (int)lane; j < K; j += 32) {
+        const uint32_t key = W.keys[j];
+        const uint32_t b = (key - g.base) >> g.s;
+        atomicAdd(&W.lut[b].y, 1u);
+        W.lut[b].x = key;   // meaningful only when the bucket holds exactly one key
+    }
+    __syncwarp();
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t run = 0u;
+#pragma unroll 4
+    for (int c = 0; c < kLutBuckets / 32; ++c) {
+        const int b = c * 32 + (int)lane;
+        const uint2 e = W.lut[b];
+        const uint32_t cnt = e.y;
+        uint32_t excl, total;
+        if (__any_sync(0xFFFFFFFFu, cnt >= 4u)) {
+            uint32_t x = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+                if ((int)lane >= d) x += y;
+            }
+            excl = x - cnt;
+            total = __shfl_sync(0xFFFFFFFFu, x, 31);
+        } else {
+            const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, cnt & 1u), b1 = __ballot_sync(0xFFFFFFFFu, cnt & 2u);
+            excl = __popc(b0 & lt) + 2u * __popc(b1 & lt);
+            total = __popc(b0) + 2u * __popc(b1);
+        }
+        W.lut[b] = make_uint2(cnt == 1u ? e.x : 0xFFFFFFFFu, (run + excl) * rowbytes | (cnt >= 2u ? 4u : 0u));
+        run += total;
     }
     __syncwarp();
 }
@@ -346,6 +444,20 @@ struct U8x {                     // eight per-request words, passed by value
     uint32_t v[8];
 };
 
+// Element k (runtime) of eight registers, and its replacement, as select
+// cascades: lets the rare paths run as rolled loops (small code) without
+// dynamically indexed -- hence local-memory -- register arrays.
+__device__ __forceinline__ uint32_t sel8(const U8x &x, int k) {
+    uint32_t r = x.v[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) r = (k == j) ? x.v[j] : r;
+    return r;
+}
+__device__ __forceinline__ void set8(U8x &x, int k, uint32_t val) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x.v[j] = (k == j) ? val : x.v[j];
+}
+
 // Selection draws of the 8 requests of group v (local requests 8v..8v+7;
 // reading L10: counter (g>>2, 0, 0), word g&3).
 __device__ __forceinline__ void group_draws_blk(uint64_t blk, const SimArgs &a, U8x &w) {
@@ -393,18 +505,20 @@ __device__ __forceinline__ uint32_t group_offsets(const U8x &w, const WarpSmem &
     return eor;
 }
 
-// exact offsets for the draws that fell in multi-key buckets (rare; inline:
-// a call would make the warp wait for its in-flight prefetch loads)
+// exact offsets for the draws that fell in multi-key buckets (rare; inline
+// -- a call would make the warp wait for its in-flight prefetch loads -- and
+// rolled, to keep the hot loop's code small)
 __device__ __forceinline__ void fix_offsets(const U8x &w, U8x &off, const uint32_t *keys, int P, LutGeom geo,
                                             uint32_t rowbytes, uint32_t lane_base) {
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < 8; ++k) {
-        const uint32_t d = max(w.v[k], geo.base);
+        const uint32_t wk = sel8(w, k);
+        const uint32_t d = max(wk, geo.base);
         if (lds64(geo.bias + ((d >> geo.s) << 3)).y & 4u) {
             int pos = 0;
 #pragma unroll 1
-            for (int step = P >> 1; step > 0; step >>= 1) pos += (keys[pos + step - 1] < w.v[k]) ? step : 0;
-            off.v[k] = lane_base + (uint32_t)pos * rowbytes;
+            for (int step = P >> 1; step > 0; step >>= 1) pos += (keys[pos + step - 1] < wk) ? step : 0;
+            set8(off, k, lane_base + (uint32_t)pos * rowbytes);
         }
     }
 }
@@ -465,32 +579,52 @@ constexpr uint32_t kBigTok = 0xF000F000u;
 // the 64-bit path if it had a token >= 4096.  Stores happen in request
 // order, so two requests of the group hitting the same row are serialised
 // through shared memory correctly.
+// packed increment of word pair p of request k
 template <int N, bool FLAGS>
-__device__ __forceinline__ void rmw_row(const Group<N, FLAGS> &g, int k, uint32_t addr, uint32_t &acc0,
-                                        uint32_t &acc) {
+__device__ __forceinline__ uint2 packed_inc(const Group<N, FLAGS> &g, int k, int p) {
     constexpr int NW = Words<N>::NW;
+    uint2 inc;
+    if (p == 0) {
+        const uint32_t w0 = plane_word<N, FLAGS>(g, 0, k);
+        inc.x = ((k & 1) ? (w0 >> 16) : (w0 & 0xFFFFu)) + (1u << kW0Shift);
+    } else {
+        inc.x = packed_hi<N, FLAGS>(g, 2 * p, k);
+    }
+    inc.y = (2 * p + 1 < NW) ? packed_hi<N, FLAGS>(g, 2 * p + 1, k) : 0u;
+    return inc;
+}
+
+// Read-modify-write of the rows of requests k, k+1 (k even): both loads issue
+// together; if the two requests hit the same row, the second store carries
+// both increments (stores stay in request order, so it lands last).
+template <int N, bool FLAGS>
+__device__ __forceinline__ void rmw_pair(const Group<N, FLAGS> &g, int k, uint32_t ra, uint32_t rb, uint32_t &acc0,
+                                         uint32_t &acc) {
     constexpr int NP = Words<N>::NP;
+    const bool same = ra == rb;
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        uint2 cur = lds64(addr + p * 256);
-        if (p == 0) {
-            const uint32_t w0 = plane_word<N, FLAGS>(g, 0, k);
-            cur.x += ((k & 1) ? (w0 >> 16) : (w0 & 0xFFFFu)) + (1u << kW0Shift);
-        } else {
-            cur.x += packed_hi<N, FLAGS>(g, 2 * p, k);
-        }
-        if (2 * p + 1 < NW) cur.y += packed_hi<N, FLAGS>(g, 2 * p + 1, k);
-        sts64(addr + p * 256, cur);
-        if (p == 0) { acc0 |= cur.x; acc |= cur.y; } else { acc |= cur.x | cur.y; }
+        uint2 A = lds64(ra + p * 256);
+        const uint2 Bl = lds64(rb + p * 256);
+        const uint2 ia = packed_inc<N, FLAGS>(g, k, p), ib = packed_inc<N, FLAGS>(g, k + 1, p);
+        A.x += ia.x;
+        A.y += ia.y;
+        uint2 B = same ? A : Bl;
+        B.x += ib.x;
+        B.y += ib.y;
+        sts64(ra + p * 256, A);
+        sts64(rb + p * 256, B);
+        if (p == 0) { acc0 |= B.x | A.x; acc |= B.y | A.y; } else { acc |= A.x | A.y | B.x | B.y; }
     }
 }
 
-// The read-modify-write chain of a group (request k's load may alias
-// request k-1's store, so the 8 updates are serialised through shared
-// memory) interleaved, in program order, with the bucket-table lookups of
-// the lane's next group: each lookup issues right behind a store and its
-// result is only needed in the next iteration, so it fills the chain's
-// load-latency gaps instead of running before it.  Returns the guard bits.
+// The read-modify-write chain of a group (a request's load may alias an
+// earlier request's store, so updates are serialised through shared memory,
+// two requests per link) interleaved, in program order, with the
+// bucket-table lookups of the lane's next group: each lookup issues right
+// behind a store and its result is only needed in the next iteration, so it
+// fills the chain's load-latency gaps instead of running before it.
+// Returns the guard bits.
 template <int N, bool FLAGS, int MODE>
 __device__ __forceinline__ uint32_t update_fast(const Group<N, FLAGS> &g, const U8x &row, uint32_t lane_base,
                                                 const U8x &wn, const WarpSmem &W, int P, LutGeom geo,
@@ -498,47 +632,57 @@ __device__ __forceinline__ uint32_t update_fast(const Group<N, FLAGS> &g, const 
     uint32_t acc0 = 0u, acc = 0u;
     if (MODE == kModeLut) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            rmw_row<N, FLAGS>(g, k, row.v[k], acc0, acc);
+        for (int k = 0; k < 8; k += 2) {
+            rmw_pair<N, FLAGS>(g, k, row.v[k], row.v[k + 1], acc0, acc);
             on.v[k] = lut_offset(wn.v[k], geo, rowbytes, lane_base, en);
+            on.v[k + 1] = lut_offset(wn.v[k + 1], geo, rowbytes, lane_base, en);
         }
     } else {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) rmw_row<N, FLAGS>(g, k, row.v[k], acc0, acc);
+        for (int k = 0; k < 8; k += 2) rmw_pair<N, FLAGS>(g, k, row.v[k], row.v[k + 1], acc0, acc);
         en = group_offsets<MODE>(wn, W, P, geo, rowbytes, lane_base, on);
     }
     return (acc0 & kGuard0) | (acc & kGuard);
 }
 
+// token of request k (runtime) at level i
+template <int N, bool FLAGS>
+__device__ __forceinline__ uint32_t token_rt(const Group<N, FLAGS> &g, int i, int k) {
+    const uint4 &u = g.t[i];
+    const int h = k >> 1;
+    const uint32_t wd = h == 0 ? u.x : h == 1 ? u.y : h == 2 ? u.z : u.w;
+    return (k & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+}
+
 // Rare paths, inline (a call would make the warp wait for its in-flight
-// prefetch loads): revert a fast update (exact: 32-bit word arithmetic is modular) and add the
+// prefetch loads) and rolled over the 8 requests (small code).
+// Revert a fast update (exact: 32-bit word arithmetic is modular) and add the
 // group's requests into the 64-bit accumulators instead ...
 template <int N, bool FLAGS>
 __device__ __forceinline__ void redo_wide(const Group<N, FLAGS> &g, const U8x &row, uint32_t lane_base,
-                                          unsigned long long *wide,
-                                       uint32_t rowbytes, uint32_t discard_off) {
+                                          unsigned long long *wide, uint32_t rowbytes, uint32_t discard_off) {
     constexpr int NW = Words<N>::NW;
     constexpr int NP = Words<N>::NP;
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < 8; ++k) {
-        const uint32_t addr = row.v[k];
+        const uint32_t r = sel8(row, k);
+        uint32_t tk[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) tk[i] = token_rt<N, FLAGS>(g, i, k);
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
-            uint2 cur = lds64(addr + p * 256);
-            if (p == 0) {
-                const uint32_t w0 = plane_word<N, FLAGS>(g, 0, k);
-                cur.x -= ((k & 1) ? (w0 >> 16) : (w0 & 0xFFFFu)) + (1u << kW0Shift);
-            } else {
-                cur.x -= packed_hi<N, FLAGS>(g, 2 * p, k);
-            }
-            if (2 * p + 1 < NW) cur.y -= packed_hi<N, FLAGS>(g, 2 * p + 1, k);
-            sts64(addr + p * 256, cur);
+            uint2 cur = lds64(r + p * 256);
+            cur.x -= (p == 0) ? tk[0] + (1u << kW0Shift) : (tk[2 * p - 1] | ((2 * p <= N - 1 ? tk[2 * p] : 0u) << 16));
+            if (2 * p + 1 < NW) cur.y -= tk[2 * p + 1] | ((2 * p + 2 <= N - 1 ? tk[2 * p + 2] : 0u) << 16);
+            sts64(r + p * 256, cur);
+        }
+        if (r != lane_base + discard_off) {
+            unsigned long long *wr = wide + (size_t)((r - lane_base) / rowbytes) * (N + 1);
+            wide_add(&wr[0], 1u);
+#pragma unroll
+            for (int i = 0; i < N; ++i) wide_add(&wr[1 + i], tk[i]);
         }
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-        if (row.v[k] != lane_base + discard_off)
-            add_wide<N, FLAGS>(wide, g, (int)((row.v[k] - lane_base) / rowbytes), k);
 }
 
 // ... and spill every row of the group with a guard bit set
@@ -546,9 +690,9 @@ template <int N>
 __device__ __forceinline__ void spill_group(const U8x &row, uint2 *hist, unsigned long long *wide, uint32_t lane,
                                             uint32_t rowbytes, uint32_t lane_base) {
     constexpr int NP = Words<N>::NP;
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < 8; ++k) {
-        const int entry = (int)((row.v[k] - lane_base) / rowbytes);
+        const int entry = (int)((sel8(row, k) - lane_base) / rowbytes);
         uint32_t acc = 0u;
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
@@ -1158,12 +1302,15 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
     // prep (also resets the queue and trace_status)
     {
         int64_t blocks = (a.n_segments + kPrepWarps - 1) / kPrepWarps;
-        if (blocks > 148 * 16) blocks = 148 * 16;
+        if (blocks > 148 * 32) blocks = 148 * 32;
         if (blocks < 1) blocks = 1;
-        const size_t smem = (size_t)kPrepWarps * 2 * (plan.sort_cap > 0 ? plan.sort_cap : 1) * 4;
-        cudaError_t e = cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const int E = plan.sort_cap <= 32 ? 1 : plan.sort_cap <= 64 ? 2 : plan.sort_cap <= 128 ? 4 : 0;
+        const int scap = E > 0 ? 32 * E : (plan.sort_cap > 0 ? plan.sort_cap : 1);
+        const size_t smem = (size_t)kPrepWarps * 2 * scap * 4;
+        auto kern = E == 1 ? prep_kernel<1> : E == 2 ? prep_kernel<2> : E == 4 ? prep_kernel<4> : prep_kernel<0>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        prep_kernel<<<(unsigned)blocks, 32 * kPrepWarps, smem, stream>>>(a);
+        kern<<<(unsigned)blocks, 32 * kPrepWarps, smem, stream>>>(a);
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         ++*launches;
