@@ -215,6 +215,7 @@ def run_sprout(args):
     import torch
     import torch.distributed as dist
     from paper_2403_12900_b200 import sprout as S
+    from paper_2403_12900_b200.collective import allreduce_totals, max_over_ranks
     from paper_2403_12900_b200.runner import Sweep
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -247,8 +248,7 @@ def run_sprout(args):
         if ev is not None:
             ev[1].record(stream)
         sw.reduce(); launches[0] += S.last_launch_count()
-        if world > 1:
-            dist.all_reduce(sw.group)
+        allreduce_totals(sw.group)      # the path's one exchange step (NCCL over NVLink for N > 1)
 
     for _ in range(args.warmup):
         if flush:
@@ -277,11 +277,7 @@ def run_sprout(args):
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
     sim_ms = [a.elapsed_time(b) for a, b in sim_ev]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(step_ms), dev)
     ms_per_step = total_ms / args.steps
 
     # LP cells/s: the solve kernel alone
@@ -291,11 +287,7 @@ def run_sprout(args):
         sw.solve()
     lp_ev[1].record(stream)
     torch.cuda.synchronize()
-    lp_ms = lp_ev[0].elapsed_time(lp_ev[1]) / args.steps
-    lp_t = torch.tensor([lp_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(lp_t, op=dist.ReduceOp.MAX)
-    lp_ms = float(lp_t.item())
+    lp_ms = max_over_ranks(lp_ev[0].elapsed_time(lp_ev[1]) / args.steps, dev)
 
     status = int(sw.totals.trace_status.item())
     g = sw.group.cpu().numpy()
@@ -355,6 +347,7 @@ def run_e2e(args, w, sh, sw, dev, world):
     import torch
     import torch.distributed as dist
     from paper_2403_12900_b200 import sprout as S
+    from paper_2403_12900_b200.collective import allreduce_totals, max_over_ranks
 
     P = w.prob
     tok_dev = sw.trace.tokens
@@ -393,15 +386,11 @@ def run_e2e(args, w, sh, sw, dev, world):
         S.sweep_host(lp, tr, cm, out, st, ws)
         if world > 1:
             g = torch.from_numpy(out).to(dev)
-            dist.all_reduce(g)
+            allreduce_totals(g)
             out[:] = g.cpu().numpy()
     ev1.record(stream)
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1) / steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / steps, dev)
     h2d = (tok_host.numel() * 2 + (fl_host.numel() if fl_host is not None else 0) + (sh.n_segments + 1) * 8
            + P.k0.size * 8 + (P.e.size + P.p.size + P.q.size + P.xi.size + 2 * P.R) * 8)
     d2h = out.size * 8 + 4

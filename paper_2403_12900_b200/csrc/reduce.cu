@@ -45,7 +45,6 @@ __global__ void __launch_bounds__(kRedThreads) reduce_stage1(const __grid_consta
 #pragma unroll
         for (int k = 0; k < K; ++k) acc[k] = 0.0;
         if (j < a.X) {
-#pragma unroll 4
             for (int64_t t = t_lo + q; t < t_hi; t += Q) {
                 const int64_t s = r * a.T + t;
                 if (s < seg_lo || s >= seg_hi) continue;
