@@ -477,7 +477,14 @@ __device__ __forceinline__ uint32_t lut_offset(uint32_t w, LutGeom geo, uint32_t
     const uint32_t d = max(w, geo.base);
     const uint2 e = lds64(geo.bias + ((d >> geo.s) << 3));
     eor |= e.y;
-    return e.y + lane_base + (d > e.x ? rowbytes : 0u);
+    uint32_t r;   // e.y + lane_base + (d > e.x ? rowbytes : 0): one compare, one select, one 3-input add
+    asm("{\n\t.reg .pred p;\n\t.reg .u32 t;\n\t"
+        "setp.gt.u32 p, %1, %2;\n\t"
+        "selp.u32 t, %3, 0, p;\n\t"
+        "add.u32 t, t, %4;\n\t"
+        "add.u32 %0, t, %5;\n\t}"
+        : "=r"(r) : "r"(d), "r"(e.x), "r"(rowbytes), "r"(e.y), "r"(lane_base));
+    return r;
 }
 
 // Shared addresses (lane_base + bin * rowbytes) of the histogram rows of the 8 draws.
