@@ -24,6 +24,7 @@
 // Segments the fast path cannot represent (more than kcap distinct
 // breakpoints; arbitrary user thresholds) use a generic per-cell path.
 #include <cuda_runtime.h>
+#include <type_traits>
 #include "sprout_device.cuh"
 #include "sprout_kernels.cuh"
 
@@ -984,15 +985,17 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
     const uint32_t n_mine = v0 < ge ? (uint32_t)((ge - v0 + 31) >> 5) : 0u;   // this lane's groups
     if (n_mine == 0) return;
     // Per-lane cursors advanced by one warp iteration (32 groups) per body:
-    // token plane 0 at the lane's current group (planes i > 0 at + i * pitch),
-    // flags, and the Philox block of the group two iterations ahead.
-    const uint8_t *tp = reinterpret_cast<const uint8_t *>(a.tokens) + (size_t)v0 * 16u;
-    const size_t pb = (size_t)a.pitch * 2u;
+    // one pointer per token plane at the lane's current group (so the next
+    // group's load and the prefetch are immediate offsets), flags, and the
+    // Philox block of the group two iterations ahead.
+    const uint8_t *qp[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) qp[q] = reinterpret_cast<const uint8_t *>(a.tokens + (size_t)q * a.pitch) + (size_t)v0 * 16u;
     const uint8_t *fp = FLAGS ? a.flags + (size_t)v0 * 8u : nullptr;
     uint64_t blk = ((a.first_request + (uint64_t)v0 * 8u) >> 2) + 128u;
     auto load_at = [&](Group<N, FLAGS> &g, int it) {   // group of iteration (current + it)
 #pragma unroll
-        for (int i = 0; i < N; ++i) g.t[i] = __ldcs(reinterpret_cast<const uint4 *>(tp + i * pb) + 32 * it);
+        for (int q = 0; q < N; ++q) g.t[q] = __ldcs(reinterpret_cast<const uint4 *>(qp[q]) + 32 * it);
         if (FLAGS) g.f = __ldcs(reinterpret_cast<const uint2 *>(fp) + 32 * it);
     };
 
@@ -1002,7 +1005,9 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
     // for v+64 (into wq[b^1]).  The three chains -- Philox rounds, table
     // lookups, histogram read-modify-writes -- are mutually independent
     // inside a body.  All rare work (a token >= 4096, a guard bit, a
-    // multi-key bucket) sits behind one branch per body.
+    // multi-key bucket) sits behind one branch per body; the prefetch and
+    // the next load are predicated, and the loop runs whole body pairs with
+    // a one-body tail, so a body has no other branch.
     Group<N, FLAGS> g[2];
     U8x oc[2], wq[2];
     load_at(g[0], 0);
@@ -1013,37 +1018,41 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
         if (MODE == kModeLut && (e & 4u)) fix_offsets(w, oc[0], W.keys, P, geo, rowbytes, lane_base);
         group_draws_blk(blk - 64u, a, wq[0]);
     }
-    for (uint32_t i0 = 0; i0 < n_mine; i0 += 2) {
+    auto body = [&](auto bc, uint32_t i) {
+        constexpr int b = decltype(bc)::value;
+        {
+            const uint32_t pf = (i + kPrefetchIters < n_mine) ? 1u : 0u;
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            const uint32_t i = i0 + b;
-            if (i < n_mine) {
-                if (i + kPrefetchIters < n_mine)
-#pragma unroll
-                    for (int q = 0; q < N; ++q)
-                        prefetch_l2(reinterpret_cast<const uint4 *>(tp + q * pb) + 32 * kPrefetchIters);
-                if (i + 1 < n_mine) load_at(g[b ^ 1], 1);
-                group_draws_blk(blk, a, wq[b ^ 1]);
-                U8x row;
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    row.v[k] = row_of<FLAGS>(oc[b].v[k], g[b].f, k, pin_row, class_bytes, a.NC, discard_row, err);
-                uint32_t en = 0u;
-                const uint32_t acc =
-                    update_fast<N, FLAGS, MODE>(g[b], row, lane_base, wq[b], W, P, geo, rowbytes, oc[b ^ 1], en);
-                const uint32_t big = group_or<N, FLAGS>(g[b]) & kBigTok;
-                if (big | acc | (MODE == kModeLut ? (en & 4u) : 0u)) {
-                    if (big) redo_wide<N, FLAGS>(g[b], row, lane_base, W.wide, rowbytes, discard_row - lane_base);
-                    if (acc) spill_group<N>(row, W.hist, W.wide, lane, rowbytes, lane_base);
-                    if (MODE == kModeLut && (en & 4u))
-                        fix_offsets(wq[b], oc[b ^ 1], W.keys, P, geo, rowbytes, lane_base);
-                }
-                tp += 512;
-                if (FLAGS) fp += 256;
-                blk += 64u;
-            }
+            for (int q = 0; q < N; ++q)
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p prefetch.global.L2 [%1];\n\t}"
+                             ::"r"(pf), "l"(qp[q] + 512 * kPrefetchIters));
         }
+        if (i + 1 < n_mine) load_at(g[b ^ 1], 1);
+        group_draws_blk(blk, a, wq[b ^ 1]);
+        U8x row;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            row.v[k] = row_of<FLAGS>(oc[b].v[k], g[b].f, k, pin_row, class_bytes, a.NC, discard_row, err);
+        uint32_t en = 0u;
+        const uint32_t acc =
+            update_fast<N, FLAGS, MODE>(g[b], row, lane_base, wq[b], W, P, geo, rowbytes, oc[b ^ 1], en);
+        const uint32_t big = group_or<N, FLAGS>(g[b]) & kBigTok;
+        if (big | acc | (MODE == kModeLut ? (en & 4u) : 0u)) {
+            if (big) redo_wide<N, FLAGS>(g[b], row, lane_base, W.wide, rowbytes, discard_row - lane_base);
+            if (acc) spill_group<N>(row, W.hist, W.wide, lane, rowbytes, lane_base);
+            if (MODE == kModeLut && (en & 4u)) fix_offsets(wq[b], oc[b ^ 1], W.keys, P, geo, rowbytes, lane_base);
+        }
+#pragma unroll
+        for (int q = 0; q < N; ++q) qp[q] += 512;
+        if (FLAGS) fp += 256;
+        blk += 64u;
+    };
+    uint32_t i = 0;
+    for (; i + 2 <= n_mine; i += 2) {
+        body(std::integral_constant<int, 0>{}, i);
+        body(std::integral_constant<int, 1>{}, i + 1);
     }
+    if (i < n_mine) body(std::integral_constant<int, 0>{}, i);
 }
 
 template <int N, bool FLAGS>
