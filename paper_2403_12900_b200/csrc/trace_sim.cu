@@ -662,6 +662,16 @@ __device__ __forceinline__ uint32_t token_rt(const Group<N, FLAGS> &g, int i, in
     return (k & 1) ? (wd >> 16) : (wd & 0xFFFFu);
 }
 
+// packed word m of one request from its tokens tk[0..N-1] (word 0 with the
+// count increment; see the row layout above)
+template <int N>
+__device__ __forceinline__ uint32_t word_of_tokens(const uint32_t (&tk)[N], int m) {
+    if (m == 0) return tk[0] + (1u << kW0Shift);
+    const uint32_t lo = tk[2 * m - 1];
+    const uint32_t hi = (2 * m <= N - 1) ? tk[2 * m] : 0u;
+    return lo | (hi << 16);
+}
+
 // Rare paths, inline (a call would make the warp wait for its in-flight
 // prefetch loads) and rolled over the 8 requests (small code).
 // Revert a fast update (exact: 32-bit word arithmetic is modular) and add the
@@ -680,8 +690,8 @@ __device__ __forceinline__ void redo_wide(const Group<N, FLAGS> &g, const U8x &r
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             uint2 cur = lds64(r + p * 256);
-            cur.x -= (p == 0) ? tk[0] + (1u << kW0Shift) : (tk[2 * p - 1] | ((2 * p <= N - 1 ? tk[2 * p] : 0u) << 16));
-            if (2 * p + 1 < NW) cur.y -= tk[2 * p + 1] | ((2 * p + 2 <= N - 1 ? tk[2 * p + 2] : 0u) << 16);
+            cur.x -= word_of_tokens<N>(tk, 2 * p);
+            if (2 * p + 1 < NW) cur.y -= word_of_tokens<N>(tk, 2 * p + 1);
             sts64(r + p * 256, cur);
         }
         if (r != lane_base + discard_off) {
@@ -924,6 +934,76 @@ __device__ __forceinline__ void readout(const SimArgs &a, const WarpSmem &W, int
     __syncwarp();
 }
 
+// The requests of a segment outside its whole groups of 8 (head: up to the
+// first 8-aligned index, tail: after the last), at most 14, one per lane:
+// each lane draws its request's word, finds its bin and adds it into its own
+// lane-private row (tokens >= 4096 go to the 64-bit accumulators).  All lanes
+// work at once, so a short segment does not serialise on two lanes.
+template <int N, bool FLAGS, int MODE>
+__device__ __forceinline__ void process_ends(const SimArgs &a, const WarpSmem &W, int64_t s0, int64_t s1, int P,
+                                             LutGeom geo, uint32_t &err) {
+    constexpr int NW = Words<N>::NW;
+    constexpr int NP = Words<N>::NP;
+    constexpr uint32_t rowbytes = NP * 256;
+    const uint32_t lane = lane_id();
+    const int64_t h_end = min(s1, (s0 + 7) & ~(int64_t)7);
+    const int64_t t_beg = max(h_end, s1 & ~(int64_t)7);
+    const int n_head = (int)(h_end - s0), n_tail = (int)(s1 - t_beg);
+    int64_t r = -1;
+    if ((int)lane < n_head) r = s0 + lane;
+    else if (lane >= 8 && (int)lane < 8 + n_tail) r = t_beg + (lane - 8);
+    if (r < 0) return;
+    const uint64_t gidx = a.first_request + (uint64_t)r;
+    const uint64_t blk = gidx >> 2;
+    const Philox4 d = philox4x32_10_rk((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, a.rk0, a.rk1);
+    const uint32_t k3 = (uint32_t)(gidx & 3u);
+    const uint32_t w = k3 == 0 ? d.v[0] : k3 == 1 ? d.v[1] : k3 == 2 ? d.v[2] : d.v[3];
+    int bin;
+    if (MODE == kModeLut) {
+        const uint32_t dd = max(w, geo.base);
+        const uint2 e = lds64(geo.bias + ((dd >> geo.s) << 3));
+        bin = (e.y & 4u) ? find_bin(W.keys, P, w) : (int)(e.y / rowbytes) + (dd > e.x ? 1 : 0);
+    } else {
+        bin = find_bin(W.keys, P, w);
+    }
+    int entry = bin;
+    if (FLAGS) {
+        const uint32_t fb = a.flags[r];
+        const int cls = (int)((fb >> 1) & 3u);
+        if (fb & 1u) entry = a.nb - 1;
+        entry += cls * a.nb;
+        if (cls >= a.NC) {
+            err |= SPROUT_TRACE_BAD_CLASS;
+            return;
+        }
+    }
+    uint32_t tk[N];
+    uint32_t big = 0u;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        tk[i] = a.tokens[(size_t)i * a.pitch + r];
+        big |= tk[i];
+    }
+    if (big >= 4096u) {
+        unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
+        wide_add(&wr[0], 1u);
+#pragma unroll
+        for (int i = 0; i < N; ++i) wide_add(&wr[1 + i], tk[i]);
+        return;
+    }
+    const uint32_t addr = smem_u32(W.hist) + lane * 8u + (uint32_t)entry * rowbytes;
+    uint32_t guard = 0u;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        uint2 cur = lds64(addr + p * 256);
+        cur.x += word_of_tokens<N>(tk, 2 * p);
+        if (2 * p + 1 < NW) cur.y += word_of_tokens<N>(tk, 2 * p + 1);
+        sts64(addr + p * 256, cur);
+        guard |= (p == 0 ? (cur.x & kGuard0) : (cur.x & kGuard)) | (cur.y & kGuard);
+    }
+    if (guard) spill_entry<N>(W.hist, W.wide, entry, lane);
+}
+
 // L2 prefetch distance of the streaming loop, in warp iterations (one
 // iteration = 32 groups = 512 contiguous bytes per token plane)
 constexpr int kPrefetchIters = 8;
@@ -959,23 +1039,7 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
     };
     for (int it = 1; it < kPrefetchIters; ++it)
         if (gf + lane + 32 * it < ge) prefetch_group(gf + lane + 32 * it);
-    {
-        const int64_t head = s0 >> 3, tail = s1 >> 3;
-        const bool has_head = (s0 & 7) != 0;
-        const bool has_tail = (s1 & 7) != 0 && !(has_head && tail == head);
-        int64_t v = 0;
-        int lo = 0, hi = 0;
-        if (lane == 0 && has_head) {
-            v = head; lo = (int)(s0 & 7); hi = (int)((s1 - (head << 3)) < 8 ? s1 - (head << 3) : 8);
-        } else if (lane == 1 && has_tail) {
-            v = tail; lo = 0; hi = (int)(s1 & 7);
-        }
-        if (hi > lo) {
-            Group<N, FLAGS> g;
-            load_group<N, FLAGS>(g, a, v);
-            process_partial<N, FLAGS, MODE>(g, v, lo, hi, a, W, P, geo, err);
-        }
-    }
+    process_ends<N, FLAGS, MODE>(a, W, s0, s1, P, geo, err);
     constexpr uint32_t rowbytes = Words<N>::NP * 256;
     const uint32_t lane_base = smem_u32(W.hist) + lane * 8u;
     const uint32_t discard_row = lane_base + (uint32_t)(a.NC * a.nb) * rowbytes;
@@ -1071,15 +1135,54 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
     __syncthreads();
 
     uint32_t err = 0u;
+    // Segment pipeline (hides the per-segment global round trips, which
+    // dominate for short segments): the queue ticket for the segment after
+    // next is taken while the current one is processed (lane 0 holds it until
+    // needed), and the next segment's metadata and keys are loaded into
+    // registers one segment ahead.
+    constexpr int kKeyRegs = 4;   // keys prefetched per lane (kcap <= 128)
+    struct SegPre {
+        int64_t sl, s0, s1;
+        int meta;
+        double k0;
+        uint32_t key[kKeyRegs];
+    };
+    auto load_pre = [&](int64_t sl) {
+        SegPre p;
+        p.sl = sl;
+        p.meta = -3;
+        p.s0 = p.s1 = 0;
+        p.k0 = 0.0;
+#pragma unroll
+        for (int t = 0; t < kKeyRegs; ++t) p.key[t] = 0xFFFFFFFFu;
+        if (sl < a.n_segments) {
+            p.meta = a.seg_meta[sl];
+            p.s0 = a.seg_offsets[sl];
+            p.s1 = a.seg_offsets[sl + 1];
+            p.k0 = a.k0[a.first_segment + sl];
+            if (a.kcap > 0 && a.kcap <= 32 * kKeyRegs) {
+#pragma unroll
+                for (int t = 0; t < kKeyRegs; ++t) {
+                    const int i = (int)lane + 32 * t;
+                    if (i < a.kcap) p.key[t] = a.seg_keys[sl * a.kcap + i];
+                }
+            }
+        }
+        return p;
+    };
+    uint32_t ticket = 0u;
+    if (lane == 0) ticket = atomicAdd(a.queue, 1u);
+    SegPre cur = load_pre((int64_t)__shfl_sync(0xFFFFFFFFu, ticket, 0));
+    if (lane == 0) ticket = atomicAdd(a.queue, 1u);
     for (;;) {
-        int64_t sl = 0;
-        if (lane == 0) sl = (int64_t)atomicAdd(a.queue, 1u);
-        sl = __shfl_sync(0xFFFFFFFFu, sl, 0);
+        const int64_t sl = cur.sl;
         if (sl >= a.n_segments) break;
+        const SegPre nxt = load_pre((int64_t)__shfl_sync(0xFFFFFFFFu, ticket, 0));
+        if (lane == 0 && nxt.sl < a.n_segments) ticket = atomicAdd(a.queue, 1u);
         const int64_t s = a.first_segment + sl;
-        const int meta = a.seg_meta[sl];
+        const int meta = cur.meta;
         const double *qrow = a.q + (a.profile_per_interval ? s : s / a.T) * N;
-        const double kp = a.k0[s] * a.pue;
+        const double kp = cur.k0 * a.pue;
 
         if (meta == -2) {   // invalid offsets: segment skipped, outputs zero
             err |= SPROUT_TRACE_BAD_OFFSETS;
@@ -1087,9 +1190,10 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
             for (int i = lane; i < NC; i += 32) { a.seg_count[sl * NC + i] = 0ull; a.seg_pinned[sl * NC + i] = 0ull; }
             for (int i = lane; i < NC * N; i += 32) a.seg_tok[sl * NC * N + i] = 0ull;
             if (lane < 4) a.seg_base[sl * 4 + lane] = 0.0;
+            cur = nxt;
             continue;
         }
-        const int64_t s0 = a.seg_offsets[sl], s1 = a.seg_offsets[sl + 1];
+        const int64_t s0 = cur.s0, s1 = cur.s1;
         if (meta == -1) {
             slow_segment<N, FLAGS>(a, W, sl, s0, s1, err);
             cell_epilogue<N>(a, W, sl, 0, kp, qrow, false, cost);
@@ -1101,12 +1205,21 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
                 W.wide[(size_t)(c * nb + rem / (N + 1)) * (N + 1) + rem % (N + 1)] = 0ull;
             }
             __syncwarp();
+            cur = nxt;
             continue;
         }
         const int K = meta;
         int P = 1;
         while (P < K + 1) P <<= 1;
-        for (int i = lane; i < P; i += 32) W.keys[i] = i < K ? a.seg_keys[sl * a.kcap + i] : 0xFFFFFFFFu;
+        if (a.kcap <= 32 * kKeyRegs) {
+#pragma unroll
+            for (int t = 0; t < kKeyRegs; ++t) {
+                const int i = (int)lane + 32 * t;
+                if (i < P) W.keys[i] = i < K ? cur.key[t] : 0xFFFFFFFFu;
+            }
+        } else {
+            for (int i = lane; i < P; i += 32) W.keys[i] = i < K ? a.seg_keys[sl * a.kcap + i] : 0xFFFFFFFFu;
+        }
         __syncwarp();
         if (a.lut && K >= kLutMinKeys && s1 - s0 >= kLutMinRequests) {
             const LutGeom geo = lut_geometry(W, K);
@@ -1129,6 +1242,7 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
             W.wide[(size_t)(c * nb + (b <= K + 1 ? b : nb - 1)) * (N + 1) + f] = 0ull;
         }
         __syncwarp();
+        cur = nxt;
     }
     err = __reduce_or_sync(0xFFFFFFFFu, err);
     if (lane == 0 && err) atomicOr(a.trace_status, err);

@@ -160,21 +160,29 @@ def test_empty_and_ragged_segments():
     check_full(w)
 
 
-def test_large_tokens_take_careful_path():
-    w = _custom(N=4000, T=5, R=1)
+@pytest.mark.parametrize("n,X,N,T", [(3, 4, 4000, 5),       # short segments: search mode
+                                     (3, 40, 90_000, 4),    # bucket-table (LUT) mode, n = 3
+                                     (5, 12, 60_000, 4),    # LUT mode, two word pairs per row
+                                     (8, 10, 40_000, 4)])   # LUT mode, n = 8
+def test_large_tokens_take_careful_path(n, X, N, T):
+    # tokens >= 4096 cannot take the packed 16/20-bit fast path: the group is
+    # reverted and added through the 64-bit accumulators (every row layout)
+    w = _custom(n=n, X=X, N=N, T=T, R=1)
     sh = synth.shard(w.spec, 1, 0)
     toks, flags = synth.host_trace(w.spec, sh)
     rng = np.random.default_rng(5)
-    idx = rng.integers(0, sh.n_requests, 200)
-    toks[rng.integers(0, 3, 200), idx] = rng.integers(32768, 65536, 200)
+    for lo, hi in ((32768, 65536), (4096, 8192)):
+        idx = rng.integers(0, sh.n_requests, 200)
+        toks[rng.integers(0, n, 200), idx] = rng.integers(lo, hi, 200)
     toks[:, 17] = 65535
+    toks[:, sh.n_requests - 1] = 40000          # a tail request
     sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=flags)
     sw.step()
     sw.simulate(levels=True)
     torch.cuda.synchronize()
     got = sw.host()
     sim = oracle_shard(w, sh, toks, flags, levels=True)
-    compare_sim(got, sim, w.prob.X, 1, 3)
+    compare_sim(got, sim, w.prob.X, 1, n)
     np.testing.assert_array_equal(got["levels"][:, :sh.n_requests], sim["levels"][:, :sh.n_requests])
 
 
