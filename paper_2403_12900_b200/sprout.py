@@ -16,7 +16,9 @@ from typing import Optional
 import numpy as np
 import torch
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsprout.so")
+# SPROUT_LIB_NAME selects another in-tree build of the same library (A/B
+# timing of kernel variants during development); default libsprout.so.
+_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("SPROUT_LIB_NAME", "libsprout.so"))
 if not os.path.exists(_LIB_PATH):
     raise ImportError(f"{_LIB_PATH} is missing: build it with `python -m paper_2403_12900_b200.build` "
                       "(there is no CPU fallback)")
