@@ -16,9 +16,18 @@ __global__ void __launch_bounds__(256) lp_solve_kernel(LpArgs a) {
     const int64_t n_cells = a.n_segments * (int64_t)a.X;
     for (int64_t cell = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cell < n_cells;
          cell += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = a.first_segment + cell / a.X;
-        const int j = (int)(cell % a.X);
-        const int64_t r = s / a.T;
+        int64_t s, r;
+        int j;
+        if (a.small) {
+            const uint32_t c32 = (uint32_t)cell, sl = a.div_x.div(c32);
+            j = (int)(c32 - sl * a.div_x.d);
+            s = a.first_segment + sl;
+            r = a.div_t.div((uint32_t)s);
+        } else {
+            s = a.first_segment + cell / a.X;
+            j = (int)(cell % a.X);
+            r = s / a.T;
+        }
         const int64_t row = a.profile_per_interval ? s : r;
 
         const double k0 = a.k0[s], kmin = a.kmin[r], kmax = a.kmax[r], xi = a.xi[j];
@@ -139,8 +148,13 @@ __global__ void __launch_bounds__(256) lp_solve_kernel(LpArgs a) {
     }
 }
 
-cudaError_t launch_lp_solve(const LpArgs &a, cudaStream_t stream, int *launches) {
+cudaError_t launch_lp_solve(const LpArgs &args, cudaStream_t stream, int *launches) {
+    LpArgs a = args;
     const int64_t n_cells = a.n_segments * (int64_t)a.X;
+    a.small = (n_cells < (int64_t)0xFFFFFFFFll && a.first_segment + a.n_segments < (int64_t)0xFFFFFFFFll &&
+               a.T < (int64_t)0xFFFFFFFFll) ? 1 : 0;
+    a.div_x = FastDiv((uint32_t)a.X);
+    a.div_t = FastDiv(a.T < (int64_t)0xFFFFFFFFll ? (uint32_t)a.T : 1u);
     if (n_cells == 0) return cudaSuccess;
     const int threads = 256;
     int64_t blocks = (n_cells + threads - 1) / threads;

@@ -27,7 +27,7 @@ static inline __host__ __device__ int red_xp(int X) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(kRedThreads) reduce_stage1(const __grid_constant__ ReduceArgs a) {
+__global__ void __launch_bounds__(kRedThreads, 4) reduce_stage1(const __grid_constant__ ReduceArgs a) {
     constexpr int K = 11 + 2 * N;
     __shared__ double red[kRedThreads];
     const int xp = red_xp(a.X), Q = kRedThreads / xp;

@@ -16,6 +16,24 @@ constexpr int kLutMinKeys = 8;      // fewer keys: level-synchronous binary sear
 constexpr int kLutMaxKeys = 511;    // larger key sets use the binary search
 constexpr int kLutMinRequests = 4096;  // shorter segments do not amortise the table build
 
+// Unsigned 32-bit division by a runtime-constant divisor d >= 1 via a
+// precomputed multiplier (Granlund-Montgomery, round-up variant):
+// q = (t + ((n - t) >> 1)) >> (l - 1), t = umulhi(m, n); exact for all n < 2^32.
+struct FastDiv {
+    uint32_t d, m, l;
+    __host__ __device__ FastDiv() : d(1), m(0), l(0) {}
+    __host__ explicit FastDiv(uint32_t div) : d(div) {
+        l = 0;
+        while (l < 32 && (1ull << l) < div) ++l;
+        m = (uint32_t)(((1ull << 32) * ((1ull << l) - div)) / div + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        if (l == 0) return n;
+        const uint32_t t = __umulhi(m, n);
+        return (t + ((n - t) >> 1)) >> (l - 1);
+    }
+};
+
 struct LpArgs {
     int n, X;
     int64_t T, first_segment, n_segments;
@@ -26,6 +44,8 @@ struct LpArgs {
     uint8_t *vertex;
     uint32_t *threshold;
     uint8_t *max_level, *cell_status;
+    FastDiv div_x, div_t;      // by X and by T (used when the cell and segment indices fit in 32 bits)
+    int small;                 // 1: n_cells and first_segment + n_segments < 2^32
 };
 
 // Simulation plan shared by the prep and the streaming kernels.
@@ -77,6 +97,7 @@ struct SimArgs {
     int lut;                   // 1: per-warp bucket table (kLutBuckets entries) for big segments
     size_t warp_smem;
     uint32_t rk0[10], rk1[10]; // Philox round keys of the selection seed
+    FastDiv div_nt;            // by n - 1 (thresholds per cell)
     CostConst cost;
 };
 

@@ -114,8 +114,8 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(const __grid_cons
                 const int idx = (int)lane * E + e;
                 v[e] = 0u;
                 if (idx < M) {
-                    const int64_t cell = sl * X + idx / nt;
-                    if (a.cell_status[cell] == SPROUT_CELL_OK) v[e] = a.threshold[cell * nt + idx % nt];
+                    const int64_t cell = sl * X + (int)a.div_nt.div((uint32_t)idx);
+                    if (a.cell_status[cell] == SPROUT_CELL_OK) v[e] = a.threshold[sl * M + idx];
                 }
             }
             warp_bitonic_sort<E>(v, lane);
@@ -1421,6 +1421,7 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
     a.sort_cap = plan.sort_cap;
     a.warp_smem = plan.warp_smem;
     a.lut = plan.lut;
+    a.div_nt = FastDiv((uint32_t)(plan.n > 1 ? plan.n - 1 : 1));
     {
         uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
         for (int r = 0; r < 10; ++r) {
