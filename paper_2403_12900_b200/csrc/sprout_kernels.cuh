@@ -98,6 +98,8 @@ struct SimArgs {
     size_t warp_smem;
     uint32_t rk0[10], rk1[10]; // Philox round keys of the selection seed
     FastDiv div_nt;            // by n - 1 (thresholds per cell)
+    FastDiv div_t;             // by T (region of a segment), valid when T < 2^32
+    int seg_batch;             // segments per queue ticket
     CostConst cost;
 };
 

@@ -891,30 +891,35 @@ __device__ __forceinline__ void readout(const SimArgs &a, const WarpSmem &W, int
     const uint32_t lane = lane_id();
     const int NC = a.NC, nb = a.nb;
     const int used = K + 2;   // draw bins 0..K and the pinned bin
-    for (int e = lane; e < NC * used; e += 32) {
-        const int c = e / used, b = e % used;
-        const int entry = c * nb + (b <= K ? b : nb - 1);
-        unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
+    {
+        for (int e = lane; e < NC * used; e += 32) {
+            int c = 0, b = e;   // (class, bin) of entry e without a division (NC <= 4)
+            while (b >= used) { b -= used; ++c; }
+            {
+                const int entry = c * nb + (b <= K ? b : nb - 1);
+                unsigned long long *wr = W.wide + (size_t)entry * (N + 1);
 #pragma unroll
-        for (int p = 0; p < NP; ++p) {
-            uint2 *row = W.hist + ((size_t)entry * NP + p) * 32;
-            uint32_t s[4] = {0u, 0u, 0u, 0u};
+                for (int p = 0; p < NP; ++p) {
+                    uint2 *row = W.hist + ((size_t)entry * NP + p) * 32;
+                    uint32_t sv[4] = {0u, 0u, 0u, 0u};
 #pragma unroll 8
-            for (int q = 0; q < 32; ++q) {
-                const int idx = (q + (int)lane) & 31;   // rotated: conflict-free
-                const uint2 val = row[idx];
-                row[idx] = make_uint2(0u, 0u);
-                s[0] += p == 0 ? (val.x & kW0Low) : (val.x & 0xFFFFu);
-                s[1] += p == 0 ? (val.x >> kW0Shift) : (val.x >> 16);
-                s[2] += val.y & 0xFFFFu;
-                s[3] += val.y >> 16;
-            }
+                    for (int q = 0; q < 32; ++q) {
+                        const int idx = (q + (int)lane) & 31;   // rotated: conflict-free
+                        const uint2 val = row[idx];
+                        row[idx] = make_uint2(0u, 0u);
+                        sv[0] += p == 0 ? (val.x & kW0Low) : (val.x & 0xFFFFu);
+                        sv[1] += p == 0 ? (val.x >> kW0Shift) : (val.x >> 16);
+                        sv[2] += val.y & 0xFFFFu;
+                        sv[3] += val.y >> 16;
+                    }
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int m = 2 * p + h;
-                if (m >= NW) break;
-                wr[word_lo_field(m)] += s[2 * h];
-                if (word_hi_field(m) <= N) wr[word_hi_field(m)] += s[2 * h + 1];
+                    for (int h = 0; h < 2; ++h) {
+                        const int m = 2 * p + h;
+                        if (m >= NW) break;
+                        wr[word_lo_field(m)] += sv[2 * h];
+                        if (word_hi_field(m) <= N) wr[word_hi_field(m)] += sv[2 * h + 1];
+                    }
+                }
             }
         }
     }
@@ -1170,18 +1175,32 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
         }
         return p;
     };
-    uint32_t ticket = 0u;
-    if (lane == 0) ticket = atomicAdd(a.queue, 1u);
-    SegPre cur = load_pre((int64_t)__shfl_sync(0xFFFFFFFFu, ticket, 0));
-    if (lane == 0) ticket = atomicAdd(a.queue, 1u);
+    // Queue tickets hand out batches of a.seg_batch consecutive segments (one
+    // atomic per batch: with many short segments a per-segment atomic on a
+    // single counter serialises in L2).  Lane 0 holds the ticket of the
+    // batch after the current one until it is needed.
+    const int64_t B = a.seg_batch;
+    int64_t it_seg = 0, it_end = 0;
+    uint32_t pend = 0u;
+    if (lane == 0) pend = atomicAdd(a.queue, 1u);
+    auto next_segment = [&]() -> int64_t {
+        if (it_seg >= it_end) {
+            it_seg = (int64_t)__shfl_sync(0xFFFFFFFFu, pend, 0) * B;
+            it_end = min(it_seg + B, a.n_segments);
+            if (it_seg >= a.n_segments) return a.n_segments;
+            if (lane == 0) pend = atomicAdd(a.queue, 1u);
+        }
+        return it_seg++;
+    };
+    SegPre cur = load_pre(next_segment());
     for (;;) {
         const int64_t sl = cur.sl;
         if (sl >= a.n_segments) break;
-        const SegPre nxt = load_pre((int64_t)__shfl_sync(0xFFFFFFFFu, ticket, 0));
-        if (lane == 0 && nxt.sl < a.n_segments) ticket = atomicAdd(a.queue, 1u);
+        const SegPre nxt = load_pre(next_segment());
         const int64_t s = a.first_segment + sl;
         const int meta = cur.meta;
-        const double *qrow = a.q + (a.profile_per_interval ? s : s / a.T) * N;
+        const double *qrow =
+            a.q + (a.profile_per_interval ? s : (s < 0xFFFFFFFFll ? (int64_t)a.div_t.div((uint32_t)s) : s / a.T)) * N;
         const double kp = cur.k0 * a.pue;
 
         if (meta == -2) {   // invalid offsets: segment skipped, outputs zero
@@ -1229,18 +1248,28 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
             stream_segment<N, FLAGS, kModeSearch>(a, W, s0, s1, P, LutGeom{0u, 32 - kLutBits, 0u}, err);
         }
         __syncwarp();
+        // the next segment's first and last groups, while this one's epilogue runs
+        if (nxt.sl < a.n_segments && nxt.meta >= -1 && nxt.s1 > nxt.s0 && nxt.s1 - nxt.s0 < 2048) {
+            const int64_t v = (lane < 16) ? (nxt.s0 >> 3) + lane : ((nxt.s1 - 1) >> 3) - (int64_t)(lane - 16);
+            if (v >= (nxt.s0 >> 3) && v <= ((nxt.s1 - 1) >> 3)) {
+#pragma unroll
+                for (int i = 0; i < N; ++i)
+                    prefetch_l2(reinterpret_cast<const uint4 *>(a.tokens + (size_t)i * a.pitch) + v);
+                if (FLAGS) prefetch_l2(a.flags + (size_t)v * 8);
+            }
+        }
         readout<N>(a, W, K);
         cell_epilogue<N>(a, W, sl, K, kp, qrow, true, cost);
         __syncwarp();
         write_seg_stats<N>(a, W, sl, kp, qrow[0], K + 1, nb - 1, true, cost);
         __syncwarp();
         // clear the rows used by this segment: draw bins 0..K+1 and the pinned bin
-        for (int e = lane; e < NC * (K + 3) * (N + 1); e += 32) {
-            const int c = e / ((K + 3) * (N + 1));
-            const int rem = e % ((K + 3) * (N + 1));
-            const int b = rem / (N + 1), f = rem % (N + 1);
-            W.wide[(size_t)(c * nb + (b <= K + 1 ? b : nb - 1)) * (N + 1) + f] = 0ull;
-        }
+        for (int c = 0; c < NC; ++c)
+            for (int b = lane; b < K + 3; b += 32) {
+                unsigned long long *wr = W.wide + (size_t)(c * nb + (b <= K + 1 ? b : nb - 1)) * (N + 1);
+#pragma unroll
+                for (int f = 0; f < N + 1; ++f) wr[f] = 0ull;
+            }
         __syncwarp();
         cur = nxt;
     }
@@ -1422,6 +1451,16 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
     a.warp_smem = plan.warp_smem;
     a.lut = plan.lut;
     a.div_nt = FastDiv((uint32_t)(plan.n > 1 ? plan.n - 1 : 1));
+    a.div_t = FastDiv(a.T < (int64_t)0xFFFFFFFFll ? (uint32_t)a.T : 1u);
+    {   // about 64 tickets per warp: one per segment for few long segments,
+        // batches of up to 32 for many short ones
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t warps = (int64_t)sms * plan.warps_per_cta;
+        int64_t bsz = a.n_segments / (warps * 64);
+        a.seg_batch = (int)(bsz < 1 ? 1 : (bsz > 8 ? 8 : bsz));
+    }
     {
         uint32_t k0 = (uint32_t)a.seed, k1 = (uint32_t)(a.seed >> 32);
         for (int r = 0; r < 10; ++r) {
