@@ -515,19 +515,27 @@ __device__ __forceinline__ uint32_t group_offsets(const U8x &w, const WarpSmem &
 
 // exact offsets for the draws that fell in multi-key buckets (rare; inline
 // -- a call would make the warp wait for its in-flight prefetch loads -- and
-// rolled, to keep the hot loop's code small)
+// rolled, to keep the hot loop's code small).  A flagged offset still
+// carries bit 2 (lane_base is 8-aligned, rows are multiples of 256 B, and a
+// multi-key entry's key is 0xFFFFFFFF so no row step was added), so the
+// flagged requests are found from registers, and the bucket's first bin is
+// (offset - lane_base) / rowbytes: the exact bin is a short linear scan over
+// the bucket's keys from there (keys are padded with 0xFFFFFFFF past K).
 __device__ __forceinline__ void fix_offsets(const U8x &w, U8x &off, const uint32_t *keys, int P, LutGeom geo,
                                             uint32_t rowbytes, uint32_t lane_base) {
+    uint32_t mask = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mask |= ((off.v[k] >> 2) & 1u) << k;
 #pragma unroll 1
-    for (int k = 0; k < 8; ++k) {
+    while (mask) {
+        const int k = __ffs(mask) - 1;
+        mask &= mask - 1u;
         const uint32_t wk = sel8(w, k);
-        const uint32_t d = max(wk, geo.base);
-        if (lds64(geo.bias + ((d >> geo.s) << 3)).y & 4u) {
-            int pos = 0;
+        uint32_t pos = (sel8(off, k) - lane_base) / rowbytes;
 #pragma unroll 1
-            for (int step = P >> 1; step > 0; step >>= 1) pos += (keys[pos + step - 1] < wk) ? step : 0;
-            set8(off, k, lane_base + (uint32_t)pos * rowbytes);
-        }
+        for (int t = 0; t < 4 && keys[pos] < wk; ++t) ++pos;
+        if (keys[pos] < wk) pos = (uint32_t)find_bin(keys, P, wk);   // crowded bucket: full search
+        set8(off, k, lane_base + pos * rowbytes);
     }
 }
 
@@ -834,22 +842,39 @@ __device__ __forceinline__ void zero_cell(const SimArgs &a, int64_t cell, int NC
 
 // Per-cell integer statistics (from the histogram prefix sums, or from the
 // slow path's global counters) and the closed-form fp64 totals of Eq. 1.
+// `pre` (N <= 3, X <= 64): the status and packed level boundaries of the
+// lane's cells lane and lane + 32 were loaded one segment ahead (SegCells).
+struct SegCells {
+    uint32_t st[2];    // cell_status
+    uint32_t bw[2];    // seg_bnd of levels 1..N-1, packed u16 (N <= 3)
+};
+
 template <int N>
 __device__ __forceinline__ void cell_epilogue(const SimArgs &a, const WarpSmem &W, int64_t sl, int K, double kp,
-                                           const double *qrow, bool fast, const CostConst &cost) {
+                                           const double *qrow, bool fast, const CostConst &cost, bool pre,
+                                           const SegCells &sc) {
     const int NC = a.NC, nb = a.nb;
-    for (int j = lane_id(); j < a.X; j += 32) {
+    int t = 0;
+    for (int j = lane_id(); j < a.X; j += 32, ++t) {
         const int64_t cell = sl * a.X + j;
-        if (a.cell_status[cell] != SPROUT_CELL_OK) {
+        const uint32_t st = pre ? (t == 0 ? sc.st[0] : sc.st[1]) : a.cell_status[cell];
+        if (st != SPROUT_CELL_OK) {
             zero_cell(a, cell, NC * N);
             continue;
         }
         int bnd[N + 1];
         bnd[0] = 0;
         bnd[N] = K + 1;
-        if (fast)
+        if (fast) {
+            if (N <= 3 && pre) {
+                const uint32_t bw = t == 0 ? sc.bw[0] : sc.bw[1];
 #pragma unroll
-            for (int L = 1; L < N; ++L) bnd[L] = a.seg_bnd[cell * (N - 1) + (L - 1)];
+                for (int L = 1; L < N; ++L) bnd[L] = (int)((bw >> (16 * (L - 1))) & 0xFFFFu);
+            } else {
+#pragma unroll
+                for (int L = 1; L < N; ++L) bnd[L] = a.seg_bnd[cell * (N - 1) + (L - 1)];
+            }
+        }
         double E = 0.0, T = 0.0, Q = 0.0;
         for (int c = 0; c < NC; ++c) {
             const unsigned long long *pre = W.wide + (size_t)(c * nb) * (N + 1);
@@ -1151,7 +1176,9 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
         int meta;
         double k0;
         uint32_t key[kKeyRegs];
+        SegCells sc;
     };
+    const bool pre_cells = N <= 3 && X <= 64;
     auto load_pre = [&](int64_t sl) {
         SegPre p;
         p.sl = sl;
@@ -1160,11 +1187,25 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
         p.k0 = 0.0;
 #pragma unroll
         for (int t = 0; t < kKeyRegs; ++t) p.key[t] = 0xFFFFFFFFu;
+        p.sc.st[0] = p.sc.st[1] = 0xFFu;
+        p.sc.bw[0] = p.sc.bw[1] = 0u;
         if (sl < a.n_segments) {
             p.meta = a.seg_meta[sl];
             p.s0 = a.seg_offsets[sl];
             p.s1 = a.seg_offsets[sl + 1];
             p.k0 = a.k0[a.first_segment + sl];
+            if (pre_cells) {
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const int j = (int)lane + 32 * t;
+                    if (j < X) {
+                        const int64_t cell = sl * X + j;
+                        p.sc.st[t] = a.cell_status[cell];
+                        p.sc.bw[t] = N == 3 ? *reinterpret_cast<const uint32_t *>(a.seg_bnd + cell * 2)
+                                   : N == 2 ? (uint32_t)a.seg_bnd[cell] : 0u;
+                    }
+                }
+            }
             if (a.kcap > 0 && a.kcap <= 32 * kKeyRegs) {
 #pragma unroll
                 for (int t = 0; t < kKeyRegs; ++t) {
@@ -1215,7 +1256,7 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
         const int64_t s0 = cur.s0, s1 = cur.s1;
         if (meta == -1) {
             slow_segment<N, FLAGS>(a, W, sl, s0, s1, err);
-            cell_epilogue<N>(a, W, sl, 0, kp, qrow, false, cost);
+            cell_epilogue<N>(a, W, sl, 0, kp, qrow, false, cost, false, cur.sc);
             __syncwarp();
             write_seg_stats<N>(a, W, sl, kp, qrow[0], 0, 1, false, cost);
             __syncwarp();
@@ -1248,18 +1289,33 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
             stream_segment<N, FLAGS, kModeSearch>(a, W, s0, s1, P, LutGeom{0u, 32 - kLutBits, 0u}, err);
         }
         __syncwarp();
-        // the next segment's first and last groups, while this one's epilogue runs
-        if (nxt.sl < a.n_segments && nxt.meta >= -1 && nxt.s1 > nxt.s0 && nxt.s1 - nxt.s0 < 2048) {
-            const int64_t v = (lane < 16) ? (nxt.s0 >> 3) + lane : ((nxt.s1 - 1) >> 3) - (int64_t)(lane - 16);
-            if (v >= (nxt.s0 >> 3) && v <= ((nxt.s1 - 1) >> 3)) {
+        // the next segment's first groups into L2 while this one's epilogue
+        // runs, so that its first loads hit L2 instead of HBM: a short
+        // segment's first and last 16 groups, a long one's first
+        // kPrefetchIters warp iterations and its last group
+        if (nxt.sl < a.n_segments && nxt.meta >= -1 && nxt.s1 > nxt.s0) {
+            const int64_t g0 = nxt.s0 >> 3, g1 = (nxt.s1 - 1) >> 3;
+            if (nxt.s1 - nxt.s0 < 2048) {
+                const int64_t v = (lane < 16) ? g0 + lane : g1 - (int64_t)(lane - 16);
+                if (v >= g0 && v <= g1) {
 #pragma unroll
-                for (int i = 0; i < N; ++i)
-                    prefetch_l2(reinterpret_cast<const uint4 *>(a.tokens + (size_t)i * a.pitch) + v);
-                if (FLAGS) prefetch_l2(a.flags + (size_t)v * 8);
+                    for (int i = 0; i < N; ++i)
+                        prefetch_l2(reinterpret_cast<const uint4 *>(a.tokens + (size_t)i * a.pitch) + v);
+                    if (FLAGS) prefetch_l2(a.flags + (size_t)v * 8);
+                }
+            } else {
+#pragma unroll 1
+                for (int it = 0; it <= kPrefetchIters; ++it) {
+                    const int64_t v = it < kPrefetchIters ? g0 + lane + 32 * it : g1;
+#pragma unroll
+                    for (int i = 0; i < N; ++i)
+                        prefetch_l2(reinterpret_cast<const uint4 *>(a.tokens + (size_t)i * a.pitch) + v);
+                    if (FLAGS) prefetch_l2(a.flags + (size_t)v * 8);
+                }
             }
         }
         readout<N>(a, W, K);
-        cell_epilogue<N>(a, W, sl, K, kp, qrow, true, cost);
+        cell_epilogue<N>(a, W, sl, K, kp, qrow, true, cost, pre_cells, cur.sc);
         __syncwarp();
         write_seg_stats<N>(a, W, sl, kp, qrow[0], K + 1, nb - 1, true, cost);
         __syncwarp();
