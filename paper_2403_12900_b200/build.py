@@ -20,6 +20,8 @@ LIB = os.path.join(PKG, "libsprout.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I" + INCLUDE, "-I" + CSRC]
+# experiments only (A/B builds): extra nvcc flags, e.g. -DSPROUT_LUT_BITS=9
+FLAGS += os.environ.get("SPROUT_NVCC_EXTRA", "").split()
 
 
 def _deps() -> list[str]:

@@ -10,7 +10,10 @@ namespace sprout {
 // bin lookup table: 2^10 buckets (64-bit entries) over the range of the keys; an entry holds
 // the bucket's single key and the histogram row offset of the bin at the bucket start
 // (see trace_sim.cu build_lut)
-constexpr int kLutBits = 10;
+#ifndef SPROUT_LUT_BITS
+#define SPROUT_LUT_BITS 10
+#endif
+constexpr int kLutBits = SPROUT_LUT_BITS;
 constexpr int kLutBuckets = 1 << kLutBits;
 constexpr int kLutMinKeys = 8;      // fewer keys: level-synchronous binary search
 constexpr int kLutMaxKeys = 511;    // larger key sets use the binary search

@@ -34,7 +34,10 @@ constexpr uint32_t kGuard = 0x80008000u;
 constexpr int kPrepWarps = 4;
 // warps per trace CTA (one CTA per SM): 8 warps = 2 per SM sub-partition leave 255 registers
 // per thread for the 4-deep load rotation and the software pipeline
-constexpr int kMaxTraceWarps = 8;
+#ifndef SPROUT_TRACE_WARPS
+#define SPROUT_TRACE_WARPS 8
+#endif
+constexpr int kMaxTraceWarps = SPROUT_TRACE_WARPS;
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
@@ -1036,7 +1039,10 @@ __device__ __forceinline__ void process_ends(const SimArgs &a, const WarpSmem &W
 
 // L2 prefetch distance of the streaming loop, in warp iterations (one
 // iteration = 32 groups = 512 contiguous bytes per token plane)
-constexpr int kPrefetchIters = 8;
+#ifndef SPROUT_PREFETCH_ITERS
+#define SPROUT_PREFETCH_ITERS 8
+#endif
+constexpr int kPrefetchIters = SPROUT_PREFETCH_ITERS;
 
 __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
