@@ -16,7 +16,7 @@
  *   3. sprout_reduce_totals: per (region, xi) and per xi group totals; the
  *      caller then all-reduces them across GPUs (NCCL, torch.distributed).
  * P:<line> cites /root/reference/PAPER.md.  Readings of silent or ambiguous
- * passages (tie-break, rounding order, RNG layout, ...) are DESIGN.md L1-L16.
+ * passages (tie-break, rounding order, RNG layout, ...) are DESIGN.md L1-L18.
  *
  * Conventions
  *   - Every array pointer inside the structs is a DEVICE pointer (cudaMalloc
@@ -234,6 +234,54 @@ sprout_status sprout_sweep_host(const sprout_lp_problem *problem, const sprout_t
 sprout_status sprout_generate_trace(const sprout_trace_generator *gen,
                                     uint16_t *tokens, int64_t plane_pitch, uint8_t *flags,
                                     sprout_stream stream);
+
+/* ---------------------------------------------------------------------- */
+/* Competing schemes of the paper's evaluation (SURVEY 8(f)
+ * NEXT-3).  Base (every request at L0) needs no solve: every
+ * simulate call reports it as the per-segment counterfactual (seg_base).
+ * The other schemes replace step 1 and reuse steps 2-3 unchanged.          */
+#define SPROUT_SCHEME_SPROUT 0       /* the directive LP of Eqs. 4-7 per (segment, xi) cell */
+#define SPROUT_SCHEME_CO2_OPT 1      /* always the lowest-carbon level */
+#define SPROUT_SCHEME_STATIC_GRID 2  /* the static configurations swept by Sprout_Sta */
+#define SPROUT_VERTEX_GRID 254       /* vertex code of a grid point with >= 2 non-zero levels */
+
+/* Step 1 for a scheme.  SPROUT: identical to sprout_solve_directives.
+ * CO2_OPT: per cell x = e_m, m = argmin_i c_i of the Eq. 2 cost vector
+ *   (ties to the lowest index, reading L17); xi is ignored (may be NULL).
+ * STATIC_GRID: cell j of every segment is point j of the simplex grid of
+ *   step 1/grid_den (x_i = k_i / grid_den, k_i >= 0 integers summing to
+ *   grid_den, ordered by k_0 descending, then k_1 descending, ...; point 0
+ *   is pure L0; reading L18); requires n_xi == sprout_static_grid_size(n,
+ *   grid_den); xi is ignored (may be NULL).
+ * For CO2_OPT and STATIC_GRID there is no quality floor: q_lb holds the
+ * mix's expected quality q.x and objective its expected carbon c.x (both
+ * summed in level order); vertex = the level of a pure mix, else
+ * SPROUT_VERTEX_GRID.  Thresholds and max_level as for SPROUT, so
+ * sprout_simulate_trace and sprout_reduce_totals apply unchanged.
+ * Errors: as sprout_solve_directives, plus INVALID_ARGUMENT for an unknown
+ * scheme, grid_den < 1 or a grid size other than n_xi. */
+sprout_status sprout_solve_scheme(const sprout_lp_problem *problem, int32_t scheme, int32_t grid_den,
+                                  const sprout_lp_solution *solution, sprout_stream stream);
+
+/* Points of the static grid, C(grid_den + n - 1, n - 1); -1 if n is outside
+ * [1,8] or grid_den < 1, or the count exceeds SPROUT_MAX_XI. */
+int64_t sprout_static_grid_size(int32_t n_levels, int32_t grid_den);
+
+/* Sprout_Sta choice ("the best static configuration is determined
+ * by sweeping the possible static configurations"; reading L18), from the
+ * group totals (device, [R+1][G][K], all segments of every region, i.e.
+ * after the cross-rank all-reduce) of a STATIC_GRID sweep.  Per region r:
+ * floor b_r = Eq. 3 at the region's mean carbon intensity (sum of k0 over
+ * its T intervals in index order, / T) with the given xi and q0 = q[r][0];
+ * point g is feasible iff  sum_L requests_L(g) * q_L >= b_r * requests(g)
+ * (realised quality, level order); choice[r] = the feasible g of least
+ * realised carbon (stat 4), ties to the lowest g (point 0, pure L0, is
+ * always feasible).  Outputs (device): choice [R] int32, x [R][n] fp64.
+ * Requires profile_per_interval == 0 and n_xi == G.  Errors:
+ * INVALID_ARGUMENT (as above, xi outside [0,1], NULL pointers); CUDA. */
+sprout_status sprout_select_static(const sprout_lp_problem *problem, int32_t grid_den, double xi,
+                                   const double *group_totals, int32_t *choice, double *x,
+                                   sprout_stream stream);
 
 /* Number of kernel launches (not memsets) the last successful call of each
  * entry point on this thread enqueued -- for launch accounting in benches. */

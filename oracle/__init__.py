@@ -87,6 +87,19 @@ def _bind(L):
     L.orc_reduce.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int64, C.c_int64,
                              _u8p, _dp, _u64p, _u64p, _dp, _dp, _dp, _dp, _u64p, _u64p, _dp, _dp]
     L.orc_reduce.restype = C.c_int
+    L.orc_solve_cells_scheme.argtypes = L.orc_solve_cells.argtypes + [C.c_int, C.c_int]
+    L.orc_solve_cells_scheme.restype = C.c_int
+    L.orc_simulate_scheme.argtypes = L.orc_simulate.argtypes + [C.c_int, C.c_int]
+    L.orc_simulate_scheme.restype = C.c_int
+    L.orc_co2opt_level.argtypes = [C.c_int, _dp]
+    L.orc_co2opt_level.restype = C.c_int
+    L.orc_grid_size.argtypes = [C.c_int, C.c_int]
+    L.orc_grid_size.restype = C.c_int64
+    L.orc_grid_point.argtypes = [C.c_int, C.c_int, C.c_int64, _dp]
+    L.orc_grid_point.restype = C.c_int
+    L.orc_select_static.argtypes = [C.c_int, C.c_int, C.c_int64, _dp, _dp, _dp, _dp, C.c_double, C.c_int,
+                                    C.c_int64, _dp, C.POINTER(C.c_int32), _dp]
+    L.orc_select_static.restype = C.c_int
     return L
 
 
@@ -156,6 +169,42 @@ def select_level(x, w: int, pinned: bool = False) -> int:
     return int(lib().orc_select_level(len(x), _p(x, _dp), int(w) & 0xFFFFFFFF, int(bool(pinned))))
 
 
+# competing schemes: scheme ids as in the C-ABI
+SCHEME_SPROUT, SCHEME_CO2_OPT, SCHEME_STATIC_GRID = 0, 1, 2
+
+
+def co2opt_level(c) -> int:
+    c = _f64(c)
+    return int(lib().orc_co2opt_level(len(c), _p(c, _dp)))
+
+
+def grid_size(n: int, D: int) -> int:
+    return int(lib().orc_grid_size(n, D))
+
+
+def grid_point(n: int, D: int, j: int):
+    x = np.zeros(n)
+    if lib().orc_grid_point(n, D, j, _p(x, _dp)) != 0:
+        raise IndexError(j)
+    return x
+
+
+def select_static(prob, xi: float, grid_den: int, group):
+    """Sprout_Sta choice per region from a sweep's group totals [R+1][G][K]."""
+    n, R, T = prob.n, prob.R, prob.T
+    assert not prob.profile_per_interval
+    G = group.shape[1]
+    group = np.ascontiguousarray(group, np.float64)
+    choice = np.zeros(R, np.int32)
+    x = np.zeros((R, n))
+    st = lib().orc_select_static(n, R, int(T), _p(_f64(prob.k0), _dp), _p(_f64(prob.kmin), _dp),
+                                 _p(_f64(prob.kmax), _dp), _p(_f64(prob.q), _dp), float(xi), int(grid_den),
+                                 int(G), _p(group, _dp), choice.ctypes.data_as(C.POINTER(C.c_int32)), _p(x, _dp))
+    if st != 0:
+        raise ValueError("oracle select_static: invalid argument")
+    return choice, x
+
+
 # --------------------------------------------------------------------------
 # whole-problem entry points.  `prob` is a synth.Problem, `cost` a
 # synth.CostModel (plain containers of numpy arrays).
@@ -167,7 +216,7 @@ def _prob_args(prob):
             float(prob.k1), float(prob.pue))
 
 
-def solve_cells(prob, first_segment: int = 0, n_segments: int | None = None):
+def solve_cells(prob, first_segment: int = 0, n_segments: int | None = None, scheme: int = 0, grid_den: int = 0):
     if n_segments is None:
         n_segments = prob.R * prob.T - first_segment
     n, X = prob.n, prob.X
@@ -177,10 +226,11 @@ def solve_cells(prob, first_segment: int = 0, n_segments: int | None = None):
         vertex=np.zeros(cells, np.uint8), threshold=np.zeros((cells, max(n - 1, 1)), np.uint64),
         max_level=np.zeros(cells, np.uint8), cell_status=np.zeros(cells, np.uint8))
     a = _prob_args(prob)
-    st = lib().orc_solve_cells(*a, int(first_segment), int(n_segments),
-                               _p(out["x"], _dp), _p(out["objective"], _dp), _p(out["q_lb"], _dp),
-                               _p(out["vertex"], _u8p), _p(out["threshold"], _u64p),
-                               _p(out["max_level"], _u8p), _p(out["cell_status"], _u8p))
+    st = lib().orc_solve_cells_scheme(*a, int(first_segment), int(n_segments),
+                                      _p(out["x"], _dp), _p(out["objective"], _dp), _p(out["q_lb"], _dp),
+                                      _p(out["vertex"], _u8p), _p(out["threshold"], _u64p),
+                                      _p(out["max_level"], _u8p), _p(out["cell_status"], _u8p),
+                                      int(scheme), int(grid_den))
     if st != 0:
         raise ValueError(f"oracle solve_cells: invalid argument (status {st})")
     out["threshold"] = out["threshold"][:, : n - 1]
@@ -188,7 +238,7 @@ def solve_cells(prob, first_segment: int = 0, n_segments: int | None = None):
 
 
 def simulate(prob, cost, seg_id, req_begin, seg_m, g0, tokens, flags=None,
-             levels: bool = False, threads: int | None = None):
+             levels: bool = False, threads: int | None = None, scheme: int = 0, grid_den: int = 0):
     """Replay the requests of the listed segments.
 
     seg_id[k]   global segment index r*T + t
@@ -219,7 +269,7 @@ def simulate(prob, cost, seg_id, req_begin, seg_m, g0, tokens, flags=None,
     if threads is None:
         threads = os.cpu_count() or 1
     ef = _f64(cost.ef); et = _f64(cost.et); pf = _f64(cost.pf); pt = _f64(cost.pt)
-    st = lib().orc_simulate(*_prob_args(prob), C.c_uint64(int(cost.seed)), int(NC),
+    st = lib().orc_simulate_scheme(*_prob_args(prob), C.c_uint64(int(cost.seed)), int(NC),
                             _p(ef, _dp), _p(et, _dp), _p(pf, _dp), _p(pt, _dp),
                             int(k), _p(seg_id, _i64p), _p(req_begin, _i64p), _p(seg_m, _i64p), _p(g0, _u64p),
                             _p(tokens, _u16p), int(pitch), _p(flags, _u8p),
@@ -227,7 +277,7 @@ def simulate(prob, cost, seg_id, req_begin, seg_m, g0, tokens, flags=None,
                             _p(out["time"], _dp), _p(out["carbon"], _dp), _p(out["quality"], _dp),
                             _p(out["seg_count"], _u64p), _p(out["seg_pinned"], _u64p),
                             _p(out["seg_tok"], _u64p), _p(out["seg_base"], _dp),
-                            _p(lv, _u8p), int(threads), C.byref(bad))
+                            _p(lv, _u8p), int(threads), C.byref(bad), int(scheme), int(grid_den))
     if st != 0:
         raise ValueError(f"oracle simulate: invalid argument (status {st})")
     out["bad_requests"] = bad.value

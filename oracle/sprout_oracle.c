@@ -217,6 +217,70 @@ int orc_select_level(int n, const double *x, uint32_t w, int pinned)
 }
 
 /* ------------------------------------------------------------------------ */
+/* Competing schemes of the evaluation.
+ * Base (all requests at L0) is the per-segment counterfactual that
+ * every run already reports.  The other two set the mix x per cell:        */
+#define ORC_SCHEME_SPROUT 0
+#define ORC_SCHEME_CO2_OPT 1
+#define ORC_SCHEME_STATIC_GRID 2
+
+/* CO2_Opt: "always use the generation directive level that
+ * yields the lowest carbon footprint", i.e. x = e_m with m = argmin_i c_i of
+ * the Eq. 2 cost vector; ties to the lowest index (reading L17).           */
+int orc_co2opt_level(int n, const double *c)
+{
+    int m = 0;
+    for (int i = 1; i < n; ++i)
+        if (c[i] < c[m]) m = i;
+    return m;
+}
+
+/* Sprout_Sta: "a single, month-long optimal generation directive
+ * configuration ... determined by sweeping the possible static
+ * configurations".  The swept configurations are the points of the simplex
+ * grid of step 1/D (reading L18): every (k_0..k_{n-1}) of non-negative
+ * integers with sum D, x_i = k_i / D, listed by k_0 descending, then k_1
+ * descending, ..., k_{n-1} = the remainder (point 0 = pure L0).  Written as
+ * the plain enumeration: walk the list in that order until point j.         */
+static int grid_walk(int i, int n, int rem, int64_t *j, int *k)
+{
+    if (i == n - 1) {
+        k[i] = rem;
+        if (*j == 0) return 1;
+        --*j;
+        return 0;
+    }
+    for (int v = rem; v >= 0; --v) {
+        k[i] = v;
+        if (grid_walk(i + 1, n, rem - v, j, k)) return 1;
+    }
+    return 0;
+}
+
+/* Number of grid points C(D + n - 1, n - 1), counted by walking the list. */
+int64_t orc_grid_size(int n, int D)
+{
+    int64_t cnt = 0;
+    int k[ORC_MAX_LEVELS];
+    for (;;) {
+        int64_t j = cnt;
+        if (!grid_walk(0, n, D, &j, k)) return cnt;
+        ++cnt;
+    }
+}
+
+/* Point j of the grid: x_i = k_i / D (IEEE division).  Returns 0, or 1 if j
+ * is past the end.                                                          */
+int orc_grid_point(int n, int D, int64_t j, double *x)
+{
+    int k[ORC_MAX_LEVELS];
+    int64_t jj = j;
+    if (j < 0 || !grid_walk(0, n, D, &jj, k)) return 1;
+    for (int i = 0; i < n; ++i) x[i] = (double)k[i] / (double)D;
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Per-cell input validation (SURVEY 8(b) cell_status code 1).               */
 static int finite_nonneg(double v) { return v >= 0.0 && v <= DBL_MAX; }
 
@@ -238,6 +302,7 @@ typedef struct {
     int64_t T;
     const double *k0, *kmin, *kmax, *xi, *e, *p, *q;
     double k1, pue;
+    int scheme, grid_den;   /* ORC_SCHEME_*; grid_den = D of the static grid */
 } orc_problem;
 
 static const double *prof(const orc_problem *P, const double *base, int64_t seg)
@@ -254,7 +319,8 @@ static int solve_cell(const orc_problem *P, int64_t seg, int j,
 {
     int n = P->n;
     int64_t r = seg / P->T;
-    double k0 = P->k0[seg], kmin = P->kmin[r], kmax = P->kmax[r], xi = P->xi[j];
+    double k0 = P->k0[seg], kmin = P->kmin[r], kmax = P->kmax[r];
+    double xi = P->scheme == ORC_SCHEME_SPROUT ? P->xi[j] : 0.0;   /* other schemes have no xi */
     const double *e = prof(P, P->e, seg), *p = prof(P, P->p, seg), *q = prof(P, P->q, seg);
     if (!cell_inputs_valid(n, k0, kmin, kmax, xi, e, p, q)) {
         for (int i = 0; i < n; ++i) x[i] = NAN;
@@ -263,9 +329,30 @@ static int solve_cell(const orc_problem *P, int64_t seg, int j,
         *max_level = 0;
         return 1;
     }
-    double b = orc_quality_lower_bound(k0, kmin, kmax, xi, q[0]);
     double c[ORC_MAX_LEVELS];
     orc_cost_vector(n, k0, P->pue, P->k1, e, p, c);
+    if (P->scheme != ORC_SCHEME_SPROUT) {
+        /* CO2_Opt: the cheapest pure level; Sprout_Sta: grid point j.  No
+         * quality floor: q_lb reports the mix's expected quality q.x and the
+         * objective its expected carbon c.x, both summed in level order.     */
+        if (P->scheme == ORC_SCHEME_CO2_OPT) {
+            int m = orc_co2opt_level(n, c);
+            for (int i = 0; i < n; ++i) x[i] = (i == m) ? 1.0 : 0.0;
+            *vertex = m;
+        } else {
+            orc_grid_point(n, P->grid_den, j, x);
+            int nz = 0, last = 0;
+            for (int i = 0; i < n; ++i) if (x[i] != 0.0) { ++nz; last = i; }
+            *vertex = nz == 1 ? last : 254;
+        }
+        double o = 0.0, qx = 0.0;
+        for (int i = 0; i < n; ++i) { o = o + c[i] * x[i]; qx = qx + q[i] * x[i]; }
+        *obj = o;
+        *qlb = qx;
+        orc_thresholds(n, x, T, max_level);
+        return 0;
+    }
+    double b = orc_quality_lower_bound(k0, kmin, kmax, xi, q[0]);
     *qlb = b;
     int st = orc_solve_lp(n, c, q, b, x, obj, vertex);
     if (st != 0) {
@@ -280,17 +367,27 @@ static int solve_cell(const orc_problem *P, int64_t seg, int j,
 /* All cells of segments [first_segment, first_segment + n_segments), cell
  * index (s - first_segment)*X + j (reading: xi innermost, SURVEY 8 notation).
  * Returns 0, or 1 on invalid scalar arguments.                              */
-int orc_solve_cells(int n, int R, int64_t T, int X,
+static int scheme_args_ok(int n, int X, int scheme, int grid_den)
+{
+    if (scheme == ORC_SCHEME_SPROUT || scheme == ORC_SCHEME_CO2_OPT) return 1;
+    if (scheme != ORC_SCHEME_STATIC_GRID || grid_den < 1) return 0;
+    return orc_grid_size(n, grid_den) == X;   /* one cell per grid point */
+}
+
+int orc_solve_cells_scheme(int n, int R, int64_t T, int X,
                     const double *k0, const double *kmin, const double *kmax, const double *xi,
                     const double *e, const double *p, const double *q, int profile_per_interval,
                     double k1, double pue, int64_t first_segment, int64_t n_segments,
                     double *x, double *objective, double *q_lb, uint8_t *vertex,
-                    uint64_t *threshold, uint8_t *max_level, uint8_t *cell_status)
+                    uint64_t *threshold, uint8_t *max_level, uint8_t *cell_status,
+                    int scheme, int grid_den)
 {
     if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1) return 1;
     if (!(pue >= 1.0 && pue <= DBL_MAX) || !(k1 >= 0.0 && k1 <= DBL_MAX)) return 1;
     if (first_segment < 0 || n_segments < 0 || first_segment + n_segments > (int64_t)R * T) return 1;
-    orc_problem P = { n, R, X, profile_per_interval, 1, T, k0, kmin, kmax, xi, e, p, q, k1, pue };
+    if (!scheme_args_ok(n, X, scheme, grid_den)) return 1;
+    orc_problem P = { n, R, X, profile_per_interval, 1, T, k0, kmin, kmax, xi, e, p, q, k1, pue,
+                      scheme, grid_den };
     for (int64_t s = 0; s < n_segments; ++s) {
         for (int j = 0; j < X; ++j) {
             int64_t cell = s * X + j;
@@ -305,6 +402,18 @@ int orc_solve_cells(int n, int R, int64_t T, int X,
         }
     }
     return 0;
+}
+
+int orc_solve_cells(int n, int R, int64_t T, int X,
+                    const double *k0, const double *kmin, const double *kmax, const double *xi,
+                    const double *e, const double *p, const double *q, int profile_per_interval,
+                    double k1, double pue, int64_t first_segment, int64_t n_segments,
+                    double *x, double *objective, double *q_lb, uint8_t *vertex,
+                    uint64_t *threshold, uint8_t *max_level, uint8_t *cell_status)
+{
+    return orc_solve_cells_scheme(n, R, T, X, k0, kmin, kmax, xi, e, p, q, profile_per_interval, k1, pue,
+                                  first_segment, n_segments, x, objective, q_lb, vertex, threshold,
+                                  max_level, cell_status, ORC_SCHEME_SPROUT, 0);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -427,7 +536,7 @@ static void *sim_worker(void *arg)
 
 /* Returns 0 ok, 1 invalid argument.  *bad_requests = requests skipped because
  * their class index (flags bits 1-2) is >= n_classes.                       */
-int orc_simulate(int n, int R, int64_t T, int X,
+int orc_simulate_scheme(int n, int R, int64_t T, int X,
                  const double *k0, const double *kmin, const double *kmax, const double *xi,
                  const double *e, const double *p, const double *q, int profile_per_interval,
                  double k1, double pue,
@@ -439,14 +548,16 @@ int orc_simulate(int n, int R, int64_t T, int X,
                  uint64_t *cnt, uint64_t *tok, double *energy, double *time_s,
                  double *carbon, double *quality,
                  uint64_t *seg_count, uint64_t *seg_pinned, uint64_t *seg_tok, double *seg_base,
-                 uint8_t *levels_out, int n_threads, int64_t *bad_requests)
+                 uint8_t *levels_out, int n_threads, int64_t *bad_requests, int scheme, int grid_den)
 {
     if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1) return 1;
     if (n_classes < 1 || n_classes > ORC_MAX_CLASSES) return 1;
+    if (!scheme_args_ok(n, X, scheme, grid_den)) return 1;
     if (!(pue >= 1.0 && pue <= DBL_MAX) || !(k1 >= 0.0 && k1 <= DBL_MAX)) return 1;
     for (int64_t k = 0; k < n_sel; ++k)
         if (seg_id[k] < 0 || seg_id[k] >= (int64_t)R * T || seg_m[k] < 0) return 1;
-    orc_problem P = { n, R, X, profile_per_interval, n_classes, T, k0, kmin, kmax, xi, e, p, q, k1, pue };
+    orc_problem P = { n, R, X, profile_per_interval, n_classes, T, k0, kmin, kmax, xi, e, p, q, k1, pue,
+                      scheme, grid_den };
     if (n_threads < 1) n_threads = 1;
     if (n_threads > 256) n_threads = 256;
     if (n_sel < n_threads) n_threads = n_sel > 0 ? (int)n_sel : 1;
@@ -469,6 +580,26 @@ int orc_simulate(int n, int R, int64_t T, int X,
     for (int t = 0; t < n_threads; ++t) bad += jobs[t].bad_requests;
     if (bad_requests) *bad_requests = bad;
     return 0;
+}
+
+int orc_simulate(int n, int R, int64_t T, int X,
+                 const double *k0, const double *kmin, const double *kmax, const double *xi,
+                 const double *e, const double *p, const double *q, int profile_per_interval,
+                 double k1, double pue,
+                 uint64_t seed, int n_classes, const double *ef, const double *et,
+                 const double *pf, const double *pt,
+                 int64_t n_sel, const int64_t *seg_id, const int64_t *req_begin,
+                 const int64_t *seg_m, const uint64_t *g0,
+                 const uint16_t *tokens, int64_t pitch, const uint8_t *flags,
+                 uint64_t *cnt, uint64_t *tok, double *energy, double *time_s,
+                 double *carbon, double *quality,
+                 uint64_t *seg_count, uint64_t *seg_pinned, uint64_t *seg_tok, double *seg_base,
+                 uint8_t *levels_out, int n_threads, int64_t *bad_requests)
+{
+    return orc_simulate_scheme(n, R, T, X, k0, kmin, kmax, xi, e, p, q, profile_per_interval, k1, pue, seed,
+                               n_classes, ef, et, pf, pt, n_sel, seg_id, req_begin, seg_m, g0, tokens, pitch,
+                               flags, cnt, tok, energy, time_s, carbon, quality, seg_count, seg_pinned, seg_tok,
+                               seg_base, levels_out, n_threads, bad_requests, ORC_SCHEME_SPROUT, 0);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -529,5 +660,44 @@ int orc_reduce(int n, int R, int64_t T, int X, int n_classes,
         for (int j = 0; j < X; ++j)
             for (int k = 0; k < K; ++k)
                 glob[(size_t)j * K + k] += out[((size_t)r * X + j) * K + k];
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Sprout_Sta selection (reading L18).  For every region r, from
+ * the group totals of a sweep over the G grid points (orc_reduce layout,
+ * [R+1][G][K]): the region's floor is Eq. 3 at its mean carbon intensity,
+ * b_r = orc_quality_lower_bound(mean_t k0[r][t], kmin_r, kmax_r, xi, q0_r)
+ * (mean = sequential sum / T); grid point g meets it iff its realised
+ * quality sum_L (requests at level L) * q_L >= b_r * (requests); the choice
+ * is the feasible point of least realised carbon (stat 4), ties to the
+ * lowest g.  Point 0 (pure L0) is always feasible.  q is per region [R][n].
+ * Outputs choice[R] and x[R][n].  Returns 0, or 1 on invalid arguments.     */
+int orc_select_static(int n, int R, int64_t T, const double *k0, const double *kmin,
+                      const double *kmax, const double *q, double xi, int grid_den,
+                      int64_t G, const double *group, int32_t *choice, double *x)
+{
+    if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || grid_den < 1) return 1;
+    if (orc_grid_size(n, grid_den) != G) return 1;
+    const int K = 11 + 2 * n;
+    for (int r = 0; r < R; ++r) {
+        double sum = 0.0;
+        for (int64_t t = 0; t < T; ++t) sum = sum + k0[(int64_t)r * T + t];
+        double kbar = sum / (double)T;
+        const double *qr = q + (size_t)r * n;
+        double b = orc_quality_lower_bound(kbar, kmin[r], kmax[r], xi, qr[0]);
+        int64_t best = -1;
+        double best_c = 0.0;
+        for (int64_t g = 0; g < G; ++g) {
+            const double *S = group + ((size_t)r * G + g) * K;
+            double Q = 0.0;
+            for (int L = 0; L < n; ++L) Q = Q + S[11 + L] * qr[L];
+            if (!(Q >= b * S[0])) continue;
+            if (best < 0 || S[4] < best_c) { best = g; best_c = S[4]; }
+        }
+        if (best < 0) best = 0;
+        choice[r] = (int32_t)best;
+        orc_grid_point(n, grid_den, best, x + (size_t)r * n);
+    }
     return 0;
 }

@@ -30,7 +30,8 @@ __global__ void __launch_bounds__(256) lp_solve_kernel(LpArgs a) {
         }
         const int64_t row = a.profile_per_interval ? s : r;
 
-        const double k0 = a.k0[s], kmin = a.kmin[r], kmax = a.kmax[r], xi = a.xi[j];
+        const double k0 = a.k0[s], kmin = a.kmin[r], kmax = a.kmax[r];
+        const double xi = a.scheme == 0 ? a.xi[j] : 0.0;   // the other schemes have no xi
         double e[N], p[N], q[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
@@ -54,6 +55,43 @@ __global__ void __launch_bounds__(256) lp_solve_kernel(LpArgs a) {
 
         if (!ok) {
             status = SPROUT_CELL_INVALID;
+        } else if (a.scheme != 0) {
+            // ---- competing schemes: no quality floor; b reports
+            // the mix's expected quality q.x, best its expected carbon c.x ----
+            const double kp = __dmul_rn(k0, a.pue);
+            double c[N];
+#pragma unroll
+            for (int i = 0; i < N; ++i) c[i] = __dadd_rn(__dmul_rn(kp, e[i]), __dmul_rn(a.k1, p[i]));
+            if (a.scheme == 1) {
+                // CO2_Opt: the cheapest level, ties to the lowest index (reading L17)
+                int m = 0;
+                double cm = c[0];
+#pragma unroll
+                for (int i = 1; i < N; ++i)
+                    if (c[i] < cm) { cm = c[i]; m = i; }
+#pragma unroll
+                for (int i = 0; i < N; ++i) x[i] = i == m ? 1.0 : 0.0;
+                best_id = m;
+            } else {
+                // Sprout_Sta sweep: grid point j of step 1/D (reading L18)
+                int k[N];
+                grid_unrank<N>(a.grid_den, j, k);
+                int nz = 0, last = 0;
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                    x[i] = __ddiv_rn((double)k[i], (double)a.grid_den);
+                    if (k[i] != 0) { ++nz; last = i; }
+                }
+                best_id = nz == 1 ? last : SPROUT_VERTEX_GRID;
+            }
+            double o = 0.0, qx = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                o = __dadd_rn(o, __dmul_rn(c[i], x[i]));
+                qx = __dadd_rn(qx, __dmul_rn(q[i], x[i]));
+            }
+            best = o;
+            b = qx;
         } else {
             // ---- Eq. 3, readings L3 and L7 ----
             double f = 0.0;

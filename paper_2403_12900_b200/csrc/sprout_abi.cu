@@ -104,6 +104,64 @@ sprout_status sprout_solve_directives(const sprout_lp_problem *problem, const sp
     return st;
 }
 
+int64_t sprout_static_grid_size(int32_t n_levels, int32_t grid_den) {
+    if (n_levels < 1 || n_levels > SPROUT_MAX_LEVELS || grid_den < 1) return -1;
+    int64_t c = 1;   // C(grid_den + n - 1, n - 1), stopping once past SPROUT_MAX_XI
+    for (int i = 1; i < n_levels; ++i) {
+        c = c * (grid_den + i) / i;
+        if (c > SPROUT_MAX_XI) return -1;
+    }
+    return c;
+}
+
+sprout_status sprout_solve_scheme(const sprout_lp_problem *problem, int32_t scheme, int32_t grid_den,
+                                  const sprout_lp_solution *solution, sprout_stream stream) {
+    if (scheme == SPROUT_SCHEME_SPROUT) return sprout_solve_directives(problem, solution, stream);
+    if (!problem || (scheme != SPROUT_SCHEME_CO2_OPT && scheme != SPROUT_SCHEME_STATIC_GRID))
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    if (scheme == SPROUT_SCHEME_STATIC_GRID &&
+        (grid_den < 1 || sprout_static_grid_size(problem->n_levels, grid_den) != (int64_t)problem->n_xi))
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    sprout_lp_problem P = *problem;
+    static const double zero = 0.0;
+    if (!P.xi) P.xi = &zero;   // not read by these schemes; keeps the shared validation
+    sprout_status st = validate_problem(&P);
+    if (st != SPROUT_OK) return st;
+    st = validate_solution(&P, solution);
+    if (st != SPROUT_OK) return st;
+    int launches = 0;
+    LpArgs a = lp_args(&P, solution);
+    a.scheme = scheme;
+    a.grid_den = scheme == SPROUT_SCHEME_STATIC_GRID ? grid_den : 0;
+    st = cuda_status(launch_lp_solve(a, reinterpret_cast<cudaStream_t>(stream), &launches));
+    if (st == SPROUT_OK) g_last_launches = launches;
+    return st;
+}
+
+sprout_status sprout_select_static(const sprout_lp_problem *problem, int32_t grid_den, double xi,
+                                   const double *group_totals, int32_t *choice, double *x, sprout_stream stream) {
+    if (!problem || !group_totals || !choice || !x) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (!(xi >= 0.0 && xi <= 1.0)) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (problem->profile_per_interval != 0) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (grid_den < 1 || sprout_static_grid_size(problem->n_levels, grid_den) != (int64_t)problem->n_xi)
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    sprout_lp_problem P = *problem;
+    static const double zero = 0.0;
+    if (!P.xi) P.xi = &zero;
+    sprout_status st = validate_problem(&P);
+    if (st != SPROUT_OK) return st;
+    if (!aligned(group_totals, 8) || !aligned(x, 8) || !aligned(choice, 4)) return SPROUT_ERR_INVALID_ARGUMENT;
+    SelectArgs a{};
+    a.n = P.n_levels; a.R = P.n_regions; a.G = P.n_xi; a.K = 11 + 2 * P.n_levels; a.grid_den = grid_den;
+    a.T = P.n_intervals;
+    a.k0 = P.k0; a.kmin = P.k0_min; a.kmax = P.k0_max; a.q = P.q; a.xi = xi;
+    a.group = group_totals; a.choice = choice; a.x = x;
+    int launches = 0;
+    st = cuda_status(launch_select_static(a, reinterpret_cast<cudaStream_t>(stream), &launches));
+    if (st == SPROUT_OK) g_last_launches = launches;
+    return st;
+}
+
 size_t sprout_workspace_bytes(const sprout_lp_problem *problem, const sprout_trace *trace) {
     if (validate_problem(problem) != SPROUT_OK) return 0;
     (void)trace;

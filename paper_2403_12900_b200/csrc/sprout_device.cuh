@@ -68,4 +68,51 @@ struct CostConst {
 
 __device__ __forceinline__ bool finite_nonneg(double v) { return v >= 0.0 && v <= 1.7976931348623157e308; }
 
+// Static-grid points (Sprout_Sta sweep; reading L18): compositions
+// (k_0..k_{n-1}) of D into n non-negative parts, ordered by k_0 descending,
+// then k_1 descending, ...  compositions(r, m) = C(r + m - 1, m - 1).
+__host__ __device__ inline int64_t compositions(int r, int m) {
+    if (m <= 1) return 1;
+    int64_t c = 1;   // C(r + m - 1, m - 1), exact: each step is an integer binomial
+    for (int i = 1; i < m; ++i) c = c * (r + i) / i;
+    return c;
+}
+
+// Unrank point j (0 <= j < compositions(D, n)) into k[0..n-1]: skip whole
+// blocks of equal k_i (largest first) by their sizes.
+__device__ inline void grid_unrank_rt(int n, int D, int64_t j, int *k) {   // runtime n (small kernels)
+    int rem = D;
+    for (int i = 0; i < n - 1; ++i) {
+        int v = rem;
+        for (;;) {
+            const int64_t block = compositions(rem - v, n - 1 - i);
+            if (j < block || v == 0) break;
+            j -= block;
+            --v;
+        }
+        k[i] = v;
+        rem -= v;
+    }
+    k[n - 1] = rem;
+    for (int i = n; i < SPROUT_MAX_LEVELS; ++i) k[i] = 0;
+}
+
+template <int N>
+__device__ __forceinline__ void grid_unrank(int D, int64_t j, int (&k)[N]) {
+    int rem = D;
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) {
+        int v = rem;
+        for (;;) {
+            const int64_t block = compositions(rem - v, N - 1 - i);   // points with k_i = v
+            if (j < block || v == 0) break;
+            j -= block;
+            --v;
+        }
+        k[i] = v;
+        rem -= v;
+    }
+    k[N - 1] = rem;
+}
+
 }  // namespace sprout

@@ -49,6 +49,18 @@ struct LpArgs {
     uint8_t *max_level, *cell_status;
     FastDiv div_x, div_t;      // by X and by T (used when the cell and segment indices fit in 32 bits)
     int small;                 // 1: n_cells and first_segment + n_segments < 2^32
+    int scheme;                // SPROUT_SCHEME_* (0 = the Sprout LP)
+    int grid_den;              // D of the static grid (scheme 2)
+};
+
+struct SelectArgs {            // Sprout_Sta choice per region (schemes.cu)
+    int n, R, G, K, grid_den;
+    int64_t T;
+    const double *k0, *kmin, *kmax, *q;
+    double xi;
+    const double *group;       // [R+1][G][K]
+    int32_t *choice;           // [R]
+    double *x;                 // [R][n]
 };
 
 // Simulation plan shared by the prep and the streaming kernels.
@@ -138,6 +150,7 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
 size_t reduce_workspace_bytes(int n, int X, int R, int64_t T, int64_t first_segment, int64_t n_segments);
 cudaError_t launch_reduce(ReduceArgs &a, void *ws, cudaStream_t stream, int *launches);
 cudaError_t launch_generate(const GenArgs &a, cudaStream_t stream, int *launches);
+cudaError_t launch_select_static(const SelectArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_check_cells(const uint8_t *status, int64_t n_cells, uint32_t *out, cudaStream_t stream, int *launches);
 
 }  // namespace sprout

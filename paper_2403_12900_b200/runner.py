@@ -26,8 +26,10 @@ class Sweep:
     local requests [shard.first_request, +n_requests)."""
 
     def __init__(self, prob, cost, shard, device, spec=None, tokens: Optional[np.ndarray] = None,
-                 flags: Optional[np.ndarray] = None, has_flags: Optional[bool] = None):
+                 flags: Optional[np.ndarray] = None, has_flags: Optional[bool] = None, scheme: int = 0,
+                 grid_den: int = 0):
         self.device = torch.device(device)
+        self.scheme, self.grid_den = int(scheme), int(grid_den)
         self.prob_host = prob
         self.dp = S.DeviceProblem.from_host(prob, self.device, shard.first_segment, shard.n_segments)
         self.sol = S.Solution.empty(self.dp)
@@ -70,7 +72,20 @@ class Sweep:
 
     # the three hot-path steps
     def solve(self, stream=None):
-        S.solve_directives(self.dp, self.sol, stream)
+        if self.scheme == S.SCHEME_SPROUT:
+            S.solve_directives(self.dp, self.sol, stream)
+        else:
+            S.solve_scheme(self.dp, self.scheme, self.grid_den, self.sol, stream)
+
+    def select_static(self, xi: float, stream=None):
+        """Sprout_Sta choice per region from this sweep's group totals (all
+        regions' segments must be local, or the totals all-reduced first)."""
+        assert self.scheme == S.SCHEME_STATIC_GRID
+        R, n = self.prob_host.R, self.prob_host.n
+        choice = torch.zeros(R, dtype=torch.int32, device=self.device)
+        x = torch.zeros((R, n), dtype=torch.float64, device=self.device)
+        S.select_static(self.dp, self.grid_den, xi, self.group, choice, x, stream)
+        return choice, x
 
     def simulate(self, levels: bool = False, stream=None):
         lv = None

@@ -98,14 +98,23 @@ _lib.sprout_generate_trace.argtypes = [_P(TraceGenerator), _vp, C.c_int64, _vp, 
 _lib.sprout_last_launch_count.restype = C.c_int32
 _lib.sprout_status_string.argtypes = [C.c_int]
 _lib.sprout_status_string.restype = C.c_char_p
+_lib.sprout_solve_scheme.argtypes = [_P(LpProblem), C.c_int32, C.c_int32, _P(LpSolution), _vp]
+_lib.sprout_static_grid_size.argtypes = [C.c_int32, C.c_int32]
+_lib.sprout_static_grid_size.restype = C.c_int64
+_lib.sprout_select_static.argtypes = [_P(LpProblem), C.c_int32, C.c_double, _vp, _vp, _vp, _vp]
 for _fn in ("sprout_solve_directives", "sprout_simulate_trace", "sprout_reduce_totals", "sprout_check_cells",
-            "sprout_sweep_host", "sprout_generate_trace"):
+            "sprout_sweep_host", "sprout_generate_trace", "sprout_solve_scheme", "sprout_select_static"):
     getattr(_lib, _fn).restype = C.c_int
 
 EXPORTS = ["sprout_solve_directives", "sprout_workspace_bytes", "sprout_simulate_trace", "sprout_group_stat_count",
            "sprout_reduce_workspace_bytes", "sprout_reduce_totals", "sprout_check_cells",
            "sprout_sweep_workspace_bytes", "sprout_sweep_host", "sprout_generate_trace",
-           "sprout_last_launch_count", "sprout_status_string"]
+           "sprout_last_launch_count", "sprout_status_string", "sprout_solve_scheme", "sprout_static_grid_size",
+           "sprout_select_static"]
+
+# competing schemes, include/sprout.h SPROUT_SCHEME_*
+SCHEME_SPROUT, SCHEME_CO2_OPT, SCHEME_STATIC_GRID = 0, 1, 2
+VERTEX_GRID = 254
 
 
 def _check(fn: str, st: int):
@@ -291,6 +300,24 @@ def reduce_totals(prob: DeviceProblem, sol: Solution, totals: Totals, n_classes:
     _check("sprout_reduce_totals",
            _lib.sprout_reduce_totals(C.byref(p), C.byref(s), C.byref(tt), int(n_classes), _ptr(group_totals),
                                      _ptr(workspace), workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def solve_scheme(prob: DeviceProblem, scheme: int, grid_den: int, sol: Solution, stream=None) -> None:
+    p, s = prob.c(), sol.c()
+    _check("sprout_solve_scheme",
+           _lib.sprout_solve_scheme(C.byref(p), int(scheme), int(grid_den), C.byref(s), _stream(stream)))
+
+
+def static_grid_size(n_levels: int, grid_den: int) -> int:
+    return int(_lib.sprout_static_grid_size(int(n_levels), int(grid_den)))
+
+
+def select_static(prob: DeviceProblem, grid_den: int, xi: float, group_totals: torch.Tensor, choice: torch.Tensor,
+                  x: torch.Tensor, stream=None) -> None:
+    p = prob.c()
+    _check("sprout_select_static",
+           _lib.sprout_select_static(C.byref(p), int(grid_den), float(xi), _ptr(group_totals), _ptr(choice),
+                                     _ptr(x), _stream(stream)))
 
 
 def check_cells(prob: DeviceProblem, sol: Solution, stream=None) -> int:

@@ -107,3 +107,30 @@ def test_workspace_size_monotone():
     b = S._lib.sprout_workspace_bytes(C.byref(_problem(S, n_segments=2)), None)
     c = S._lib.sprout_workspace_bytes(C.byref(_problem(S, n_xi=64, n_segments=2)), None)
     assert 0 < a <= b < c
+
+
+def test_static_grid_size_closed_form():
+    """sprout_static_grid_size = C(D + n - 1, n - 1) (stars and bars), -1 past SPROUT_MAX_XI."""
+    import math
+    from paper_2403_12900_b200 import sprout as S
+    for n in range(1, 9):
+        for D in range(1, 40):
+            g = math.comb(D + n - 1, n - 1)
+            assert S.static_grid_size(n, D) == (g if g <= S.MAX_XI else -1), (n, D)
+    assert S.static_grid_size(0, 5) == -1 and S.static_grid_size(3, 0) == -1
+
+
+def test_scheme_validation_rejects_without_device():
+    from paper_2403_12900_b200 import sprout as S
+    sol = S.LpSolution(16, 16, 16, 16, 16, 16, 16)
+    P = _problem(S)
+    assert S._lib.sprout_solve_scheme(C.byref(P), 7, 0, C.byref(sol), None) == 1          # unknown scheme
+    assert S._lib.sprout_solve_scheme(C.byref(P), 2, 0, C.byref(sol), None) == 1          # grid_den < 1
+    assert S._lib.sprout_solve_scheme(C.byref(P), 2, 20, C.byref(sol), None) == 1         # n_xi != 231
+    assert S._lib.sprout_solve_scheme(C.byref(_problem(S, pue=0.5)), 1, 0, C.byref(sol), None) == 1
+    G = _problem(S, n_xi=231)
+    assert S._lib.sprout_select_static(C.byref(G), 20, 1.5, 16, 16, 16, None) == 1       # xi > 1
+    assert S._lib.sprout_select_static(C.byref(G), 19, 0.1, 16, 16, 16, None) == 1       # wrong grid
+    assert S._lib.sprout_select_static(C.byref(G), 20, 0.1, None, 16, 16, None) == 1     # NULL totals
+    assert S._lib.sprout_select_static(C.byref(_problem(S, n_xi=231, profile_per_interval=1)), 20, 0.1,
+                                       16, 16, 16, None) == 1
