@@ -44,9 +44,10 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def workload_desc(w):
+def workload_desc(w, scheme="sprout"):
     P = w.prob
-    return (f"{w.name}: {P.R} regions x {P.T} CI intervals x {P.X} xi x {P.n} directive levels, "
+    cells = {"sprout": "xi", "co2opt": "CO2_Opt cell", "static": "static grid points"}[scheme]
+    return (f"{w.name}: {P.R} regions x {P.T} CI intervals x {P.X} {cells} x {P.n} directive levels, "
             f"{w.N:,} requests, {w.cost.n_classes} model class(es), flags={'yes' if w.spec.has_flags else 'no'}")
 
 
@@ -128,7 +129,7 @@ class ClockSampler:
 # ---------------------------------------------------------------- CPU oracle
 
 
-def oracle_sample_run(w, seg_ids, threads):
+def oracle_sample_run(w, seg_ids, threads, scheme=0, grid_den=0):
     """Oracle on a set of whole segments of the workload (LP + replay),
     tokens regenerated on the host (generation not timed)."""
     import oracle
@@ -145,12 +146,12 @@ def oracle_sample_run(w, seg_ids, threads):
     flags = np.concatenate(flags_parts) if w.spec.has_flags and parts else None
     t0 = time.perf_counter()
     oracle.simulate(w.prob, w.cost, np.asarray(seg_ids), np.array(begins), np.array(ms),
-                    np.array(g0s, np.uint64), toks, flags, threads=threads)
+                    np.array(g0s, np.uint64), toks, flags, threads=threads, scheme=scheme, grid_den=grid_den)
     dt = time.perf_counter() - t0
     return pos, len(seg_ids), dt
 
 
-def oracle_baseline(w, target_s=12.0):
+def oracle_baseline(w, target_s=12.0, scheme=0, grid_den=0):
     """cpu_baseline: the oracle as it stands on the host cores, on a bounded,
     deterministic segment sample of the same workload (calibrated to
     ~target_s of CPU time)."""
@@ -162,12 +163,12 @@ def oracle_baseline(w, target_s=12.0):
     m = np.diff(off)
     # calibration on a few segments
     ids = synth.sample_segments(w.spec, 0, S, every=max(1, S // max(threads, 8)))[: max(threads, 8)]
-    req, _, dt = oracle_sample_run(w, ids, threads)
+    req, _, dt = oracle_sample_run(w, ids, threads, scheme, grid_den)
     rate = req / max(dt, 1e-6)
     want = int(rate * target_s)
     every = max(1, int(np.ceil(w.N / max(want, 1))))
     ids = synth.sample_segments(w.spec, 0, S, every=every)
-    req, nseg, dt = oracle_sample_run(w, ids, threads)
+    req, nseg, dt = oracle_sample_run(w, ids, threads, scheme, grid_den)
     return {"value": req / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{nseg} whole segments (every {every}th + first/last/largest) = {req:,} requests x "
                       f"{w.prob.X} xi cells, LP solves included, token generation excluded; {dt:.2f} s",
@@ -185,7 +186,7 @@ def run_reference(args):
     S = w.prob.R * w.prob.T
     # each step: a bounded sample sized to ~2 s of host time
     ids = synth.sample_segments(w.spec, 0, S, every=max(1, S // 64))[:64]
-    req, _, dt = oracle_sample_run(w, ids, threads)
+    req, _, dt = oracle_sample_run(w, ids, threads, scheme, grid_den)
     rate = req / max(dt, 1e-6)
     every = max(1, int(np.ceil(w.N / max(int(rate * 2.0), 1))))
     ids = synth.sample_segments(w.spec, 0, S, every=every)
@@ -211,6 +212,23 @@ def run_reference(args):
 # ---------------------------------------------------------------- GPU arm
 
 
+SCHEMES = {"sprout": 0, "co2opt": 1, "static": 2}
+
+
+def scheme_workload(args):
+    """The config's workload for the chosen scheme: Sprout keeps
+    its xi cells; CO2_Opt has one cell per segment; the Sprout_Sta sweep one
+    cell per point of the simplex grid of step 1/grid_den."""
+    import dataclasses
+    import math
+    w = synth.make_workload(args.config)
+    if args.scheme == "sprout":
+        return w
+    X = 1 if args.scheme == "co2opt" else math.comb(args.grid_den + w.prob.n - 1, w.prob.n - 1)
+    prob = dataclasses.replace(w.prob, X=X, xi=np.zeros(X))
+    return dataclasses.replace(w, prob=prob, description=w.description + f" [{args.scheme}]")
+
+
 def run_sprout(args):
     import torch
     import torch.distributed as dist
@@ -228,9 +246,10 @@ def run_sprout(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    w = synth.make_workload(args.config)
+    w = scheme_workload(args)
+    scheme = SCHEMES[args.scheme]
     sh = synth.shard(w.spec, world, rank)
-    sw = Sweep(w.prob, w.cost, sh, dev, spec=w.spec)
+    sw = Sweep(w.prob, w.cost, sh, dev, spec=w.spec, scheme=scheme, grid_den=args.grid_den)
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
     trace_bytes = sw.trace.tokens.numel() * 2 + (sw.trace.flags.numel() if sw.trace.flags is not None else 0)
@@ -249,6 +268,8 @@ def run_sprout(args):
             ev[1].record(stream)
         sw.reduce(); launches[0] += S.last_launch_count()
         allreduce_totals(sw.group)      # the path's one exchange step (NCCL over NVLink for N > 1)
+        if scheme == S.SCHEME_STATIC_GRID:
+            sw.select_static(args.static_xi); launches[0] += S.last_launch_count()
 
     for _ in range(args.warmup):
         if flush:
@@ -294,7 +315,7 @@ def run_sprout(args):
 
     # e2e: the host-buffer C-ABI call (H2D of the trace + D2H of the totals timed)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and scheme == S.SCHEME_SPROUT:
         e2e = run_e2e(args, w, sh, sw, dev, world)
 
     if rank != 0:
@@ -314,13 +335,14 @@ def run_sprout(args):
             traffic = d.get("dram_bytes_per_launch")
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        cpu = oracle_baseline(w, args.cpu_seconds)
+        cpu = oracle_baseline(w, args.cpu_seconds, scheme, args.grid_den)
     N = w.N
     line = {
         "metric": METRIC, "value": N / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64/u32", "data": "synthetic",
-        "config": {"workload": workload_desc(w), "config": w.name, "requests": N, "lp_cells": w.prob.C,
+        "config": {"workload": workload_desc(w, args.scheme), "config": w.name, "scheme": args.scheme, "requests": N,
+                   "lp_cells": w.prob.C,
                    "parallelism": f"segments sharded over {world} GPU(s), one NCCL allreduce of group totals",
                    "l2": ("flushed (256 MB memset) between steps" if flush else
                           f"inputs larger than L2 (trace {trace_bytes / 1e9:.2f} GB/GPU > L2 {l2 / 1e6:.0f} MB)")},
@@ -411,6 +433,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--flush-l2", action="store_true")
+    ap.add_argument("--scheme", default="sprout", choices=sorted(SCHEMES),
+                    help="competing scheme of P:364-373 (co2opt, static = the Sprout_Sta grid sweep)")
+    ap.add_argument("--grid-den", type=int, default=20, help="static grid step 1/D (Sprout_Sta sweep)")
+    ap.add_argument("--static-xi", type=float, default=0.1, help="xi of the Sprout_Sta quality floor")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

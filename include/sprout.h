@@ -188,6 +188,24 @@ sprout_status sprout_simulate_trace(const sprout_lp_problem *problem,
                                     void *workspace, size_t workspace_bytes,
                                     sprout_stream stream);
 
+/* sprout_simulate_trace with the caller's bound on the distinct non-zero
+ * thresholds (breakpoints) of any one segment's valid cells: it sizes the
+ * per-warp histograms (more warps per SM when the bound is small).  0 = the
+ * bound of LP mixes (<= 2 non-zero levels), min(n_xi*(n-1), n_xi+1).  A
+ * segment with more breakpoints than the bound takes the generic path
+ * (correct, slower; SPROUT_TRACE_SLOW_PATH).  A STATIC_GRID sweep of step
+ * 1/D has at most 2(D-1): the cumulative sums are multiples j/D (reading
+ * L18), each rounded up to one of two adjacent integers.  Errors: as
+ * sprout_simulate_trace, plus INVALID_ARGUMENT for a negative bound. */
+sprout_status sprout_simulate_trace_bounded(const sprout_lp_problem *problem,
+                                            const sprout_lp_solution *solution,
+                                            const sprout_trace *trace,
+                                            const sprout_cost_model *cost,
+                                            const sprout_cell_totals *totals,
+                                            uint8_t *levels_out, int32_t max_breakpoints,
+                                            void *workspace, size_t workspace_bytes,
+                                            sprout_stream stream);
+
 /* Number of statistics K per group row: 11 + 2n.  Row layout: 0 requests,
  * 1 opted-out, 2 energy kWh, 3 time s, 4 carbon g, 5 quality, 6-9 Base
  * energy/time/carbon/quality, 10 expected carbon (requests x objective),

@@ -175,6 +175,16 @@ sprout_status sprout_simulate_trace(const sprout_lp_problem *problem, const spro
                                     const sprout_trace *trace, const sprout_cost_model *cost,
                                     const sprout_cell_totals *totals, uint8_t *levels_out, void *workspace,
                                     size_t workspace_bytes, sprout_stream stream) {
+    return sprout_simulate_trace_bounded(problem, solution, trace, cost, totals, levels_out, 0, workspace,
+                                         workspace_bytes, stream);
+}
+
+sprout_status sprout_simulate_trace_bounded(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                            const sprout_trace *trace, const sprout_cost_model *cost,
+                                            const sprout_cell_totals *totals, uint8_t *levels_out,
+                                            int32_t max_breakpoints, void *workspace, size_t workspace_bytes,
+                                            sprout_stream stream) {
+    if (max_breakpoints < 0) return SPROUT_ERR_INVALID_ARGUMENT;
     sprout_status st = validate_problem(problem);
     if (st == SPROUT_OK) st = validate_solution(problem, solution);
     if (st == SPROUT_OK) st = validate_trace(problem, trace);
@@ -182,7 +192,8 @@ sprout_status sprout_simulate_trace(const sprout_lp_problem *problem, const spro
     if (st == SPROUT_OK) st = validate_totals(problem, totals);
     if (st != SPROUT_OK) return st;
     SimPlan plan;
-    if (!make_sim_plan(problem->n_levels, problem->n_xi, cost->n_classes, &plan)) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (!make_sim_plan(problem->n_levels, problem->n_xi, cost->n_classes, &plan, max_breakpoints))
+        return SPROUT_ERR_INVALID_ARGUMENT;
     if (!workspace || workspace_bytes < sim_workspace_bytes(plan, problem->n_segments) || !aligned(workspace, 256))
         return SPROUT_ERR_INVALID_ARGUMENT;
 

@@ -1155,6 +1155,72 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
     if (i < n_mine) body(std::integral_constant<int, 0>{}, i);
 }
 
+// A segment without breakpoints (K = 0: every valid cell's mix is pure, so
+// each cell's level is the same for every draw -- e.g. CO2_Opt, or an LP
+// whose floor is inactive) and without flags: every request is in draw bin
+// 0 whatever its draw, so no draw is needed and the bin-0 statistics are the
+// segment's request count and token sums.  Lanes sum the tokens of their
+// groups per level in registers (4 groups of 8 requests in flight per lane),
+// the warp reduces them, and lane 0 adds them to the 64-bit row of bin 0;
+// the epilogue then runs unchanged.
+template <int N>
+__device__ __forceinline__ void stream_segment_k0(const SimArgs &a, const WarpSmem &W, int64_t s0, int64_t s1) {
+    const uint32_t lane = lane_id();
+    uint64_t acc[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) acc[q] = 0ull;
+    const int64_t gf = (s0 + 7) >> 3, ge = s1 >> 3;   // full groups [gf, ge)
+    // head / tail requests (at most 7 each), one per lane
+    {
+        const int64_t h_end = min(s1, (s0 + 7) & ~(int64_t)7);
+        const int64_t t_beg = max(h_end, s1 & ~(int64_t)7);
+        int64_t r = -1;
+        if ((int64_t)lane < h_end - s0) r = s0 + lane;
+        else if (lane >= 8 && (int64_t)(lane - 8) < s1 - t_beg) r = t_beg + (lane - 8);
+        if (r >= 0) {
+#pragma unroll
+            for (int q = 0; q < N; ++q) acc[q] += a.tokens[(size_t)q * a.pitch + r];
+        }
+    }
+    auto half_sum = [](uint4 t) -> uint32_t {   // sum of the 8 u16 tokens of a 16-byte group (< 2^19)
+        return (t.x & 0xFFFFu) + (t.x >> 16) + (t.y & 0xFFFFu) + (t.y >> 16) + (t.z & 0xFFFFu) + (t.z >> 16) +
+               (t.w & 0xFFFFu) + (t.w >> 16);
+    };
+    constexpr int U = 4;   // groups in flight per lane
+    int64_t v = gf + lane;
+    for (; v + 32 * (U - 1) < ge; v += 32 * U) {
+        uint4 t[U][N];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int q = 0; q < N; ++q)
+                t[u][q] = __ldcs(reinterpret_cast<const uint4 *>(a.tokens + (size_t)q * a.pitch) + v + 32 * u);
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+            uint32_t sq = 0u;   // < 4 * 2^19
+#pragma unroll
+            for (int u = 0; u < U; ++u) sq += half_sum(t[u][q]);
+            acc[q] += sq;
+        }
+    }
+    for (; v < ge; v += 32) {
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+            acc[q] += half_sum(__ldcs(reinterpret_cast<const uint4 *>(a.tokens + (size_t)q * a.pitch) + v));
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) acc[q] += __shfl_xor_sync(0xFFFFFFFFu, acc[q], d);
+    if (lane == 0) {
+        unsigned long long *wr = W.wide;   // class 0, bin 0
+        wr[0] += (unsigned long long)(s1 - s0);
+#pragma unroll
+        for (int q = 0; q < N; ++q) wr[1 + q] += acc[q];
+    }
+    __syncwarp();
+}
+
 template <int N, bool FLAGS>
 __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __grid_constant__ SimArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -1287,7 +1353,9 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
             for (int i = lane; i < P; i += 32) W.keys[i] = i < K ? a.seg_keys[sl * a.kcap + i] : 0xFFFFFFFFu;
         }
         __syncwarp();
-        if (a.lut && K >= kLutMinKeys && s1 - s0 >= kLutMinRequests) {
+        if (!FLAGS && K == 0) {
+            stream_segment_k0<N>(a, W, s0, s1);
+        } else if (a.lut && K >= kLutMinKeys && s1 - s0 >= kLutMinRequests) {
             const LutGeom geo = lut_geometry(W, K);
             build_lut(W, K, geo, Words<N>::NP * 256);
             stream_segment<N, FLAGS, kModeLut>(a, W, s0, s1, P, geo, err);
@@ -1403,12 +1471,13 @@ static int nominal_kcap(int n, int X) {
     return (n == 1) ? 0 : (int)((M < (long)X + 1) ? M : (long)X + 1);
 }
 
-bool make_sim_plan(int n, int X, int NC, SimPlan *plan) {
+bool make_sim_plan(int n, int X, int NC, SimPlan *plan, int max_keys) {
     SimPlan p{};
     p.n = n; p.X = X; p.NC = NC;
     p.nw = 2 * (((n + 2) / 2 + 1) / 2);   // words allocated per entry: whole 64-bit pairs
     const long M = (long)X * (n - 1);
     int kcap = nominal_kcap(n, X);
+    if (max_keys > 0 && max_keys < kcap) kcap = max_keys;   // caller's bound (e.g. a static grid sweep)
     p.sort_cap = 0;
     if (M > 0) {
         long c = 1;
@@ -1505,7 +1574,7 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
     const int kc = nominal_kcap(plan.n, plan.X);
     off += ((size_t)a.n_segments * kc * 4 + 255) & ~(size_t)255;
     a.seg_bnd = reinterpret_cast<uint16_t *>(w + off);
-    a.kcap = plan.kcap < 0 ? -1 : kc;
+    a.kcap = plan.kcap;   // -1 (all slow) or the plan's bound <= kc (the seg_keys stride)
     a.nb = plan.nb;
     a.nw = plan.nw;
     a.kp = plan.kp;

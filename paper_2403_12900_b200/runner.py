@@ -93,7 +93,11 @@ class Sweep:
             if self.levels is None:
                 self.levels = torch.full((self.dp.X, self.trace.pitch), 0xFF, dtype=torch.uint8, device=self.device)
             lv = self.levels
-        S.simulate_trace(self.dp, self.sol, self.trace, self.cost, self.totals, self.ws, lv, stream)
+        if self.scheme == S.SCHEME_STATIC_GRID:   # <= 2(D-1) distinct breakpoints per segment
+            S.simulate_trace_bounded(self.dp, self.sol, self.trace, self.cost, self.totals,
+                                     max(1, 2 * (self.grid_den - 1)), self.ws, lv, stream)
+        else:
+            S.simulate_trace(self.dp, self.sol, self.trace, self.cost, self.totals, self.ws, lv, stream)
 
     def reduce(self, stream=None):
         S.reduce_totals(self.dp, self.sol, self.totals, self.n_classes, self.group, self.rws, stream)

@@ -98,19 +98,22 @@ _lib.sprout_generate_trace.argtypes = [_P(TraceGenerator), _vp, C.c_int64, _vp, 
 _lib.sprout_last_launch_count.restype = C.c_int32
 _lib.sprout_status_string.argtypes = [C.c_int]
 _lib.sprout_status_string.restype = C.c_char_p
+_lib.sprout_simulate_trace_bounded.argtypes = [_P(LpProblem), _P(LpSolution), _P(Trace), _P(CostModel),
+                                               _P(CellTotals), _vp, C.c_int32, _vp, C.c_size_t, _vp]
 _lib.sprout_solve_scheme.argtypes = [_P(LpProblem), C.c_int32, C.c_int32, _P(LpSolution), _vp]
 _lib.sprout_static_grid_size.argtypes = [C.c_int32, C.c_int32]
 _lib.sprout_static_grid_size.restype = C.c_int64
 _lib.sprout_select_static.argtypes = [_P(LpProblem), C.c_int32, C.c_double, _vp, _vp, _vp, _vp]
 for _fn in ("sprout_solve_directives", "sprout_simulate_trace", "sprout_reduce_totals", "sprout_check_cells",
-            "sprout_sweep_host", "sprout_generate_trace", "sprout_solve_scheme", "sprout_select_static"):
+            "sprout_sweep_host", "sprout_generate_trace", "sprout_solve_scheme", "sprout_select_static",
+            "sprout_simulate_trace_bounded"):
     getattr(_lib, _fn).restype = C.c_int
 
 EXPORTS = ["sprout_solve_directives", "sprout_workspace_bytes", "sprout_simulate_trace", "sprout_group_stat_count",
            "sprout_reduce_workspace_bytes", "sprout_reduce_totals", "sprout_check_cells",
            "sprout_sweep_workspace_bytes", "sprout_sweep_host", "sprout_generate_trace",
            "sprout_last_launch_count", "sprout_status_string", "sprout_solve_scheme", "sprout_static_grid_size",
-           "sprout_select_static"]
+           "sprout_select_static", "sprout_simulate_trace_bounded"]
 
 # competing schemes, include/sprout.h SPROUT_SCHEME_*
 SCHEME_SPROUT, SCHEME_CO2_OPT, SCHEME_STATIC_GRID = 0, 1, 2
@@ -283,6 +286,16 @@ def simulate_trace(prob: DeviceProblem, sol: Solution, trace: DeviceTrace, cost:
            _lib.sprout_simulate_trace(C.byref(p), C.byref(s), C.byref(t), C.byref(cost), C.byref(tt),
                                       _ptr(levels_out), _ptr(workspace), workspace.numel() * workspace.element_size(),
                                       _stream(stream)))
+
+
+def simulate_trace_bounded(prob: DeviceProblem, sol: Solution, trace: DeviceTrace, cost: CostModel, totals: Totals,
+                           max_breakpoints: int, workspace: torch.Tensor, levels_out: Optional[torch.Tensor] = None,
+                           stream=None) -> None:
+    p, s, t, tt = prob.c(), sol.c(), trace.c(), totals.c()
+    _check("sprout_simulate_trace_bounded",
+           _lib.sprout_simulate_trace_bounded(C.byref(p), C.byref(s), C.byref(t), C.byref(cost), C.byref(tt),
+                                              _ptr(levels_out), int(max_breakpoints), _ptr(workspace),
+                                              workspace.numel() * workspace.element_size(), _stream(stream)))
 
 
 def group_stat_count(n_levels: int) -> int:

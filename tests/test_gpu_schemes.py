@@ -113,3 +113,25 @@ def test_static_choice_uses_every_region_interval():
     g1 = one.group.cpu().numpy()
     for r in range(prob.R):   # identical, or a near-tie broken by the split's summation order
         assert c1[r] == c2[r] or g1[r, c1[r], 4] == pytest.approx(g1[r, c2[r], 4], rel=FP_RTOL)
+
+
+@pytest.mark.parametrize("name", ["C4", "C5"])
+def test_co2opt_parity_no_flags(name):
+    """No flags and pure mixes only: every segment takes the register path
+    (no breakpoints, no draws)."""
+    kw = dict(n_requests=400000, n_intervals=48)
+    if name == "C5":
+        kw["n_regions"] = 4
+    w = synth.make_workload(name, **kw)
+    prob = dataclasses.replace(w.prob, X=1, xi=np.zeros(1))
+    _check(w, prob, S.SCHEME_CO2_OPT, 0)
+
+
+def test_sprout_pure_segments_register_path():
+    """Sprout LP with xi = 0: the floor is q0 itself, so (q0 the unique
+    maximum) every cell is pure L0 -- the breakpoint-free register path --
+    mixed with xi = 1 cells in a second run for contrast."""
+    w = synth.make_workload("C4", n_requests=300000, n_intervals=48)
+    for xi in ([0.0], [0.0, 0.0], [0.0, 1.0]):
+        prob = dataclasses.replace(w.prob, X=len(xi), xi=np.asarray(xi, float))
+        _check(w, prob, S.SCHEME_SPROUT, 0)
