@@ -15,6 +15,9 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 for C in C2 C3 C5; do
   timeout 900 python bench.py --config $C --steps 10 --warmup 3 --no-e2e --cpu-seconds 8 > gpurun_out/bench_${C}_$TAG.json 2> gpurun_out/bench_${C}_$TAG.err; echo "bench $C rc=$?"; cut -c1-300 gpurun_out/bench_${C}_$TAG.json
 done
+for SC in co2opt static; do
+  timeout 900 python bench.py --config C4 --scheme $SC --steps 10 --warmup 3 --no-e2e --cpu-seconds 8 > gpurun_out/bench_C4_${SC}_$TAG.json 2> gpurun_out/bench_C4_${SC}_$TAG.err; echo "bench C4 $SC rc=$?"; cut -c1-300 gpurun_out/bench_C4_${SC}_$TAG.json
+done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu-launch rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:trace_kernel -s 2 -c 1 -o gpurun_out/prof_$TAG python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu-full rc=$?"
 timeout 900 ncu --set full --clock-control none -k regex:'lp_solve|prep_kernel|reduce_stage' -s 6 -c 5 -o gpurun_out/prof_other_$TAG python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_other_$TAG.log 2>&1; echo "ncu-other rc=$?"
