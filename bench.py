@@ -179,7 +179,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    w = synth.make_workload(args.config)
+    w = scheme_workload(args)
+    scheme, grid_den = SCHEMES[args.scheme], args.grid_den
     import oracle
     oracle.build()
     threads = os.cpu_count() or 1
@@ -191,17 +192,18 @@ def run_reference(args):
     every = max(1, int(np.ceil(w.N / max(int(rate * 2.0), 1))))
     ids = synth.sample_segments(w.spec, 0, S, every=every)
     for _ in range(args.warmup):
-        oracle_sample_run(w, ids, threads)
+        oracle_sample_run(w, ids, threads, scheme, grid_den)
     times, reqs = [], 0
     for _ in range(args.steps):
-        r, nseg, dt = oracle_sample_run(w, ids, threads)
+        r, nseg, dt = oracle_sample_run(w, ids, threads, scheme, grid_den)
         times.append(dt); reqs += r
     total = sum(times)
     value = reqs / total
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/u32",
-            "data": "synthetic", "config": {"workload": workload_desc(w), "sample_segments": int(len(ids))},
+            "data": "synthetic", "config": {"workload": workload_desc(w, args.scheme), "config": w.name,
+                                            "scheme": args.scheme, "sample_segments": int(len(ids))},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
                              "sample": f"{len(ids)} whole segments per step (every {every}th + first/last/largest), "
                                        f"{reqs // max(args.steps, 1):,} requests per step"},
@@ -227,6 +229,40 @@ def scheme_workload(args):
     X = 1 if args.scheme == "co2opt" else math.comb(args.grid_den + w.prob.n - 1, w.prob.n - 1)
     prob = dataclasses.replace(w.prob, X=X, xi=np.zeros(X))
     return dataclasses.replace(w, prob=prob, description=w.description + f" [{args.scheme}]")
+
+
+def run_evaluator(args):
+    """The opportunistic evaluator trigger sweep (Eq. 8; NEXT-2) on
+    the config's CI traces: 64 urgencies x 64 thresholds per region, one
+    sequential scan per configuration (one thread each)."""
+    import torch
+    from paper_2403_12900_b200 import sprout as S
+    w = synth.make_workload(args.config, n_requests=1000)
+    P = w.prob
+    dt = 1.0 / 12 if args.config == "C3" else 1.0
+    dev = torch.device("cuda", 0)
+    betas, thetas = np.linspace(0.0, 0.1, 64), np.linspace(0.05, 1.0, 64)
+    k2 = torch.as_tensor(P.k0, dtype=torch.float64, device=dev)
+    kmax = torch.as_tensor(P.kmax, dtype=torch.float64, device=dev)
+    out = torch.zeros((P.R, 64, 64, 4), dtype=torch.float64, device=dev)
+    run = lambda: S.evaluator_sweep(k2, kmax, P.T, dt, betas, thetas, 6.0, 3, 0.2778, P.pue, out)
+    for _ in range(args.warmup):
+        run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        run()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    cfg = P.R * 64 * 64
+    print(json.dumps({"metric": "evaluator trigger sweep: configuration-intervals/s", "value": cfg * P.T / (ms * 1e-3),
+                      "unit": "config-intervals/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                      "ms_per_step": ms, "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+                      "config": {"workload": f"{w.name} CI traces: {P.R} regions x {P.T} intervals x 64 beta x 64 "
+                                             f"theta, grace 6 h, fallback 3", "configs": cfg},
+                      "evaluations_total": float(out[..., 0].sum().item())}))
 
 
 def run_sprout(args):
@@ -437,9 +473,14 @@ def main():
                     help="competing scheme of P:364-373 (co2opt, static = the Sprout_Sta grid sweep)")
     ap.add_argument("--grid-den", type=int, default=20, help="static grid step 1/D (Sprout_Sta sweep)")
     ap.add_argument("--static-xi", type=float, default=0.1, help="xi of the Sprout_Sta quality floor")
+    ap.add_argument("--evaluator", action="store_true",
+                    help="time the opportunistic evaluator trigger sweep (Eq. 8) instead of the hot path")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.evaluator:
+        run_evaluator(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -301,6 +301,48 @@ sprout_status sprout_select_static(const sprout_lp_problem *problem, int32_t gri
                                    const double *group_totals, int32_t *choice, double *x,
                                    sprout_stream stream);
 
+/* ---------------------------------------------------------------------- */
+/* Opportunistic evaluator trigger sweep (Eq. 8; SURVEY 8(f)
+ * NEXT-2).  The evaluation server's carbon intensity k2 is the region's CI
+ * ("it resides in the same region as the inference server").  For
+ * every (region r, urgency beta_b, threshold theta_h) configuration, one
+ * sequential scan over the region's T intervals (reading L19):
+ *   state: i0 = index of the last evaluation (the trace start counts as one),
+ *   factor f = d_b^(i - i0) by repeated multiplication, d_b = exp(-beta_b *
+ *   interval_hours) evaluated once on the host (Eq. 8's e^{-beta (t - t0)});
+ *   k'(i) = f * k2(i).  Evaluate at i iff (i - i0) * interval_hours >=
+ *   grace_hours (condition ii) AND k'(i) < theta_h * k2_max[r] (iii) AND
+ *   either k' has a trailing local minimum at i-1 (k'(i-1) < k'(i-2) and
+ *   k'(i) > k'(i-1), both samples after i0; condition i) or the last
+ *   `fallback` samples after i0 were all below the threshold (Fig. 4(b):
+ *   "the increasing evaluation urgency ensures that offline evaluation
+ *   always occurs"; 0 disables).  An evaluation at i costs
+ *   k2(i) * pue * eval_kwh gCO2 and restarts the state at i0 = i.
+ * Output (device, fp64) [R][n_beta][n_theta][4]: evaluations, their carbon
+ * (g), the longest time without an evaluation (hours, counting the trace
+ * start and end), and the sum of k2 at the evaluations.                    */
+#define SPROUT_MAX_EVAL_PARAMS 64
+typedef struct {
+    int32_t n_regions;         /* R >= 1 */
+    int32_t n_beta;            /* 1..SPROUT_MAX_EVAL_PARAMS */
+    int64_t n_intervals;       /* T >= 1 */
+    double interval_hours;     /* > 0: length of one CI interval */
+    const double *k2;          /* [R*T] device: carbon intensity, gCO2/kWh */
+    const double *k2_max;      /* [R] device: historical maximum ("50% of the historical maximum") */
+    const double *beta;        /* [n_beta] HOST: urgency, 1/hour (>= 0; P:233 uses 0.028) */
+    int32_t n_theta;           /* 1..SPROUT_MAX_EVAL_PARAMS */
+    int32_t fallback;          /* >= 0 samples (0 = local minimum only) */
+    const double *theta;       /* [n_theta] HOST: threshold as a fraction of k2_max (>= 0) */
+    double grace_hours;        /* >= 0 */
+    double eval_kwh;           /* energy of one evaluation, kWh (>= 0) */
+    double pue;                /* >= 1 */
+} sprout_evaluator_problem;
+
+/* Errors: INVALID_ARGUMENT (sizes, NULL pointers, NaN/negative parameters);
+ * CUDA.  One thread per configuration; deterministic. */
+sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *problem, double *out,
+                                     sprout_stream stream);
+
 /* Number of kernel launches (not memsets) the last successful call of each
  * entry point on this thread enqueued -- for launch accounting in benches. */
 int32_t sprout_last_launch_count(void);

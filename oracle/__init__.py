@@ -100,6 +100,9 @@ def _bind(L):
     L.orc_select_static.argtypes = [C.c_int, C.c_int, C.c_int64, _dp, _dp, _dp, _dp, C.c_double, C.c_int,
                                     C.c_int64, _dp, C.POINTER(C.c_int32), _dp]
     L.orc_select_static.restype = C.c_int
+    L.orc_evaluator_sweep.argtypes = [C.c_int, C.c_int64, C.c_double, _dp, _dp, C.c_int, _dp, C.c_int, _dp,
+                                      C.c_double, C.c_int, C.c_double, C.c_double, _dp]
+    L.orc_evaluator_sweep.restype = C.c_int
     return L
 
 
@@ -300,4 +303,19 @@ def reduce(prob, n_classes, first_segment, n_segments, cells, sim):
                           _p(sim["quality"], _dp), _p(sim["seg_count"], _u64p),
                           _p(sim["seg_pinned"], _u64p), _p(sim["seg_base"], _dp), _p(out, _dp))
     assert st == 0
+    return out
+
+
+def evaluator_sweep(k2, k2max, T: int, dt: float, betas, thetas, grace: float, fallback: int,
+                    eval_kwh: float, pue: float):
+    """Opportunistic evaluator trigger sweep (Eq. 8): out[R][B][H][4]."""
+    k2 = _f64(k2); k2max = _f64(k2max); betas = _f64(betas); thetas = _f64(thetas)
+    R = len(k2max)
+    assert k2.size == R * T
+    out = np.zeros((R, len(betas), len(thetas), 4))
+    st = lib().orc_evaluator_sweep(R, int(T), float(dt), _p(k2, _dp), _p(k2max, _dp), len(betas), _p(betas, _dp),
+                                   len(thetas), _p(thetas, _dp), float(grace), int(fallback), float(eval_kwh),
+                                   float(pue), _p(out, _dp))
+    if st != 0:
+        raise ValueError("oracle evaluator_sweep: invalid argument")
     return out

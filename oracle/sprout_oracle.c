@@ -701,3 +701,67 @@ int orc_select_static(int n, int R, int64_t T, const double *k0, const double *k
     }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Opportunistic evaluator trigger sweep (Eq. 8; reading L19).
+ * For each (region r, beta b, theta h), scan t = 1..T-1 in order with the
+ * state of the last evaluation t0 (the trace start counts as one):
+ *   Eq. 8, urgency-adjusted intensity k'(t) = e^{-beta (t - t0)} k2(t), the
+ *   factor kept as d^(t - t0) by repeated multiplication, d = exp(-beta*dt);
+ *   evaluate at t iff (ii) the grace period has elapsed, (t - t0)*dt >= grace;
+ *   (iii) k'(t) < theta * k2max_r ("below a predefined threshold, such as
+ *   50% of the historical maximum"); and (i) t-1 was a local minimum of k'
+ *   (k'(t-1) < k'(t-2), k'(t) > k'(t-1), with t-2 >= t0), or the last F
+ *   samples after t0 were all below the threshold (fallback; Fig. 4(b)).
+ * An evaluation costs k2(t) * pue * eval_kwh gCO2 (16 GPUs x 250 W x 0.5 s x
+ * 500 samples in SURVEY's accounting is the caller's eval_kwh).
+ * out[r][b][h] = {evaluations, carbon g, longest gap h (trace start and end
+ * included), sum of k2 at the evaluations}.                                 */
+int orc_evaluator_sweep(int R, int64_t T, double dt, const double *k2, const double *k2max,
+                        int B, const double *beta, int H, const double *theta,
+                        double grace, int F, double eval_kwh, double pue, double *out)
+{
+    if (R < 1 || T < 1 || B < 1 || H < 1 || F < 0 || !(dt > 0.0)) return 1;
+    for (int r = 0; r < R; ++r)
+        for (int b = 0; b < B; ++b)
+            for (int h = 0; h < H; ++h) {
+                const double *k = k2 + (int64_t)r * T;
+                double d = exp(-(beta[b] * dt));
+                double thr = theta[h] * k2max[r];
+                int64_t t0 = 0;
+                double f = 1.0;
+                /* k'(s) for the samples s since t0, recomputed from the definition */
+                double prev1 = k[0], prev2 = 0.0;
+                int64_t below = 0, gap = 0;
+                double n_eval = 0.0, carbon = 0.0, sum_k2 = 0.0;
+                for (int64_t t = 1; t < T; ++t) {
+                    f = f * d;
+                    double kp = f * k[t];
+                    int under = kp < thr;
+                    if (under) below = below + 1; else below = 0;
+                    int64_t since = t - t0;
+                    int grace_ok = (double)since * dt >= grace;
+                    int local_min = since >= 2 && prev1 < prev2 && kp > prev1;
+                    int fallback = F > 0 && below >= F;
+                    prev2 = prev1;
+                    prev1 = kp;
+                    if (grace_ok && under && (local_min || fallback)) {
+                        n_eval = n_eval + 1.0;
+                        carbon = carbon + (k[t] * pue) * eval_kwh;
+                        sum_k2 = sum_k2 + k[t];
+                        if (since > gap) gap = since;
+                        t0 = t;
+                        f = 1.0;
+                        prev1 = k[t];
+                        below = 0;
+                    }
+                }
+                if (T - t0 > gap) gap = T - t0;
+                double *o = out + (((size_t)r * B + b) * H + h) * 4;
+                o[0] = n_eval;
+                o[1] = carbon;
+                o[2] = (double)gap * dt;
+                o[3] = sum_k2;
+            }
+    return 0;
+}

@@ -162,6 +162,44 @@ sprout_status sprout_select_static(const sprout_lp_problem *problem, int32_t gri
     return st;
 }
 
+sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *P, double *out, sprout_stream stream) {
+    if (!P || !out) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (P->n_regions < 1 || P->n_intervals < 1 || P->n_beta < 1 || P->n_beta > SPROUT_MAX_EVAL_PARAMS ||
+        P->n_theta < 1 || P->n_theta > SPROUT_MAX_EVAL_PARAMS || P->fallback < 0)
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    if (!(P->interval_hours > 0.0) || !std::isfinite(P->interval_hours) || !(P->grace_hours >= 0.0) ||
+        !std::isfinite(P->grace_hours) || !(P->eval_kwh >= 0.0) || !std::isfinite(P->eval_kwh) ||
+        !(P->pue >= 1.0) || !std::isfinite(P->pue))
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    if (!P->k2 || !P->k2_max || !P->beta || !P->theta || !aligned(out, 8)) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (P->n_intervals >= ((int64_t)1 << 31)) return SPROUT_ERR_OVERFLOW;
+    EvalArgs a{};
+    {   // grace test in samples: the least s with (double)s * dt >= grace (same decision for every s)
+        double s0 = std::ceil(P->grace_hours / P->interval_hours);
+        if (s0 > 2147483647.0) s0 = 2147483647.0;
+        int64_t s = (int64_t)s0;
+        while (s > 0 && (double)(s - 1) * P->interval_hours >= P->grace_hours) --s;
+        while (s < 2147483647 && !((double)s * P->interval_hours >= P->grace_hours)) ++s;
+        a.grace_samples = (int)s;
+    }
+    a.R = P->n_regions; a.B = P->n_beta; a.H = P->n_theta; a.F = P->fallback; a.T = P->n_intervals;
+    a.dt = P->interval_hours; a.grace = P->grace_hours; a.eval_kwh = P->eval_kwh; a.pue = P->pue;
+    a.k2 = P->k2; a.k2_max = P->k2_max; a.out = out;
+    for (int b = 0; b < a.B; ++b) {
+        const double beta = P->beta[b];
+        if (!(beta >= 0.0) || !std::isfinite(beta)) return SPROUT_ERR_INVALID_ARGUMENT;
+        a.decay[b] = std::exp(-(beta * a.dt));   // Eq. 8's factor over one interval (reading L19)
+    }
+    for (int h = 0; h < a.H; ++h) {
+        if (!(P->theta[h] >= 0.0) || !std::isfinite(P->theta[h])) return SPROUT_ERR_INVALID_ARGUMENT;
+        a.theta[h] = P->theta[h];
+    }
+    int launches = 0;
+    sprout_status st = cuda_status(launch_evaluator(a, reinterpret_cast<cudaStream_t>(stream), &launches));
+    if (st == SPROUT_OK) g_last_launches = launches;
+    return st;
+}
+
 size_t sprout_workspace_bytes(const sprout_lp_problem *problem, const sprout_trace *trace) {
     if (validate_problem(problem) != SPROUT_OK) return 0;
     (void)trace;

@@ -53,6 +53,17 @@ struct LpArgs {
     int grid_den;              // D of the static grid (scheme 2)
 };
 
+struct EvalArgs {               // evaluator trigger sweep (evaluator.cu)
+    int R, B, H, F;
+    int grace_samples;         // least s >= 0 with s * dt >= grace (fp64, as the definition reads)
+    int64_t T;
+    double dt, grace, eval_kwh, pue;
+    const double *k2, *k2_max;
+    double decay[SPROUT_MAX_EVAL_PARAMS];   // exp(-beta_b * dt), host-evaluated
+    double theta[SPROUT_MAX_EVAL_PARAMS];
+    double *out;               // [R][B][H][4]
+};
+
 struct SelectArgs {            // Sprout_Sta choice per region (schemes.cu)
     int n, R, G, K, grid_den;
     int64_t T;
@@ -150,6 +161,7 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
 size_t reduce_workspace_bytes(int n, int X, int R, int64_t T, int64_t first_segment, int64_t n_segments);
 cudaError_t launch_reduce(ReduceArgs &a, void *ws, cudaStream_t stream, int *launches);
 cudaError_t launch_generate(const GenArgs &a, cudaStream_t stream, int *launches);
+cudaError_t launch_evaluator(const EvalArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_select_static(const SelectArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_check_cells(const uint8_t *status, int64_t n_cells, uint32_t *out, cudaStream_t stream, int *launches);
 

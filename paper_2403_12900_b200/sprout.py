@@ -100,20 +100,28 @@ _lib.sprout_status_string.argtypes = [C.c_int]
 _lib.sprout_status_string.restype = C.c_char_p
 _lib.sprout_simulate_trace_bounded.argtypes = [_P(LpProblem), _P(LpSolution), _P(Trace), _P(CostModel),
                                                _P(CellTotals), _vp, C.c_int32, _vp, C.c_size_t, _vp]
+class EvaluatorProblem(C.Structure):
+    _fields_ = [("n_regions", C.c_int32), ("n_beta", C.c_int32), ("n_intervals", C.c_int64),
+                ("interval_hours", C.c_double), ("k2", _vp), ("k2_max", _vp), ("beta", _vp),
+                ("n_theta", C.c_int32), ("fallback", C.c_int32), ("theta", _vp), ("grace_hours", C.c_double),
+                ("eval_kwh", C.c_double), ("pue", C.c_double)]
+
+
+_lib.sprout_evaluator_sweep.argtypes = [_P(EvaluatorProblem), _vp, _vp]
 _lib.sprout_solve_scheme.argtypes = [_P(LpProblem), C.c_int32, C.c_int32, _P(LpSolution), _vp]
 _lib.sprout_static_grid_size.argtypes = [C.c_int32, C.c_int32]
 _lib.sprout_static_grid_size.restype = C.c_int64
 _lib.sprout_select_static.argtypes = [_P(LpProblem), C.c_int32, C.c_double, _vp, _vp, _vp, _vp]
 for _fn in ("sprout_solve_directives", "sprout_simulate_trace", "sprout_reduce_totals", "sprout_check_cells",
             "sprout_sweep_host", "sprout_generate_trace", "sprout_solve_scheme", "sprout_select_static",
-            "sprout_simulate_trace_bounded"):
+            "sprout_simulate_trace_bounded", "sprout_evaluator_sweep"):
     getattr(_lib, _fn).restype = C.c_int
 
 EXPORTS = ["sprout_solve_directives", "sprout_workspace_bytes", "sprout_simulate_trace", "sprout_group_stat_count",
            "sprout_reduce_workspace_bytes", "sprout_reduce_totals", "sprout_check_cells",
            "sprout_sweep_workspace_bytes", "sprout_sweep_host", "sprout_generate_trace",
            "sprout_last_launch_count", "sprout_status_string", "sprout_solve_scheme", "sprout_static_grid_size",
-           "sprout_select_static", "sprout_simulate_trace_bounded"]
+           "sprout_select_static", "sprout_simulate_trace_bounded", "sprout_evaluator_sweep"]
 
 # competing schemes, include/sprout.h SPROUT_SCHEME_*
 SCHEME_SPROUT, SCHEME_CO2_OPT, SCHEME_STATIC_GRID = 0, 1, 2
@@ -331,6 +339,18 @@ def select_static(prob: DeviceProblem, grid_den: int, xi: float, group_totals: t
     _check("sprout_select_static",
            _lib.sprout_select_static(C.byref(p), int(grid_den), float(xi), _ptr(group_totals), _ptr(choice),
                                      _ptr(x), _stream(stream)))
+
+
+def evaluator_sweep(k2: torch.Tensor, k2_max: torch.Tensor, n_intervals: int, interval_hours: float, betas,
+                    thetas, grace_hours: float, fallback: int, eval_kwh: float, pue: float, out: torch.Tensor,
+                    stream=None) -> None:
+    """Opportunistic evaluator trigger sweep (Eq. 8); out [R][len(betas)][len(thetas)][4] fp64 device."""
+    b = np.ascontiguousarray(betas, np.float64)
+    t = np.ascontiguousarray(thetas, np.float64)
+    P = EvaluatorProblem(int(k2_max.numel()), len(b), int(n_intervals), float(interval_hours), _ptr(k2),
+                         _ptr(k2_max), b.ctypes.data, len(t), int(fallback), t.ctypes.data, float(grace_hours),
+                         float(eval_kwh), float(pue))
+    _check("sprout_evaluator_sweep", _lib.sprout_evaluator_sweep(C.byref(P), _ptr(out), _stream(stream)))
 
 
 def check_cells(prob: DeviceProblem, sol: Solution, stream=None) -> int:

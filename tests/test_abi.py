@@ -134,3 +134,22 @@ def test_scheme_validation_rejects_without_device():
     assert S._lib.sprout_select_static(C.byref(G), 20, 0.1, None, 16, 16, None) == 1     # NULL totals
     assert S._lib.sprout_select_static(C.byref(_problem(S, n_xi=231, profile_per_interval=1)), 20, 0.1,
                                        16, 16, 16, None) == 1
+
+
+def test_evaluator_validation_rejects_without_device():
+    from paper_2403_12900_b200 import sprout as S
+    b = (C.c_double * 2)(0.028, 0.0)
+    t = (C.c_double * 2)(0.5, 0.3)
+
+    def P(**kw):
+        d = dict(n_regions=1, n_beta=2, n_intervals=24, interval_hours=1.0, k2=16, k2_max=16,
+                 beta=C.addressof(b), n_theta=2, fallback=3, theta=C.addressof(t), grace_hours=6.0,
+                 eval_kwh=0.28, pue=1.2)
+        d.update(kw)
+        return S.EvaluatorProblem(*[d[f[0]] for f in S.EvaluatorProblem._fields_])
+    for kw in (dict(n_regions=0), dict(n_beta=0), dict(n_beta=65), dict(n_theta=0), dict(interval_hours=0.0),
+               dict(grace_hours=-1.0), dict(fallback=-1), dict(pue=0.9), dict(eval_kwh=float("nan")),
+               dict(k2=None), dict(beta=None)):
+        assert S._lib.sprout_evaluator_sweep(C.byref(P(**kw)), 16, None) == 1, kw
+    bad = (C.c_double * 2)(-0.1, 0.0)
+    assert S._lib.sprout_evaluator_sweep(C.byref(P(beta=C.addressof(bad))), 16, None) == 1
