@@ -158,6 +158,8 @@ cudaError_t launch_lp_solve(const LpArgs &a, cudaStream_t stream, int *launches)
 bool make_sim_plan(int n, int X, int NC, SimPlan *plan, int max_keys = 0);
 size_t sim_workspace_bytes(const SimPlan &plan, int64_t n_segments);
 cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStream_t stream, int *launches);
+bool trace_x1_supported(int n, int X, int NC);
+cudaError_t launch_trace_x1(SimArgs &a, cudaStream_t stream);
 size_t reduce_workspace_bytes(int n, int X, int R, int64_t T, int64_t first_segment, int64_t n_segments);
 cudaError_t launch_reduce(ReduceArgs &a, void *ws, cudaStream_t stream, int *launches);
 cudaError_t launch_generate(const GenArgs &a, cudaStream_t stream, int *launches);

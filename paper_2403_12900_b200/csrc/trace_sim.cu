@@ -38,6 +38,10 @@ constexpr int kPrepWarps = 4;
 #define SPROUT_TRACE_WARPS 8
 #endif
 constexpr int kMaxTraceWarps = SPROUT_TRACE_WARPS;
+#ifndef SPROUT_DISABLE_X1
+#define SPROUT_DISABLE_X1 0
+#endif
+constexpr bool kDisableX1 = SPROUT_DISABLE_X1;   // A/B only: route X = 1 through the general kernel
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
@@ -1550,7 +1554,8 @@ static cudaError_t launch_trace_t(SimArgs &a, const SimPlan &plan, cudaStream_t 
 
 template <int N>
 static cudaError_t launch_n(SimArgs &a, const SimPlan &plan, cudaStream_t stream, int *launches) {
-    cudaError_t e = a.flags ? launch_trace_t<N, true>(a, plan, stream) : launch_trace_t<N, false>(a, plan, stream);
+    cudaError_t e = (!kDisableX1 && trace_x1_supported(N, a.X, a.NC)) ? launch_trace_x1(a, stream)
+                  : a.flags ? launch_trace_t<N, true>(a, plan, stream) : launch_trace_t<N, false>(a, plan, stream);
     if (e != cudaSuccess) return e;
     ++*launches;
     if (a.levels_out) {

@@ -1,0 +1,319 @@
+// trace_x1.cu -- step 2 of the hot path for ONE cell per segment (X = 1:
+// configs C1 and C3, and any single-xi sweep) with n <= 4 levels and <= 2
+// model classes.  With a single cell the level of a request is the a6 rule
+// itself -- level = pinned ? 0 : min(#{i : w >= T_i}, max_level) (P:162,
+// P:240; reading L10) -- so no breakpoint merge or histogram is needed: a
+// warp owns a segment, each lane takes aligned quads of 4 consecutive
+// requests (one Philox4x32-10 call, 8-byte token loads, one 4-byte flags
+// load), and accumulates the cell's (class, level) counts and tokens and the
+// segment's statistics in 32-bit registers; the warp folds them with
+// __reduce_add_sync at the segment's end (in chunks, so no 32-bit sum can
+// overflow).  Short segments (C3: 190 requests on average) are bound by
+// per-segment overhead, which this keeps to a few dozen instructions instead
+// of a histogram readout.  Outputs and fp64 closed forms are those of
+// trace_sim.cu's epilogue (same formula order).
+#include <cuda_runtime.h>
+#include "sprout_device.cuh"
+#include "sprout_kernels.cuh"
+
+namespace sprout {
+
+constexpr int kX1Warps = 8;                   // warps per CTA
+constexpr int64_t kX1Chunk = (int64_t)1 << 21; // requests per fold: <= 2^16 per lane, token sums <= 2^16 * 65535 < 2^32
+
+template <int N, bool FLAGS, bool NC2>
+__global__ void __launch_bounds__(32 * kX1Warps, 3) trace_x1_kernel(const __grid_constant__ SimArgs a) {
+    __shared__ CostConst cost;
+    // per-warp 64-bit totals of a segment: [0, NC*N) cell counts, [NC*N, 2NC*N) cell tokens,
+    // then tokens per level (all classes), class-1 tokens per level, valid requests,
+    // class-1 requests, pinned per class
+    constexpr int kTot = 4 * 4 + 2 * 4 + 2 + 2;
+    __shared__ unsigned long long tot_s[kX1Warps][kTot];
+    unsigned long long *tot = tot_s[threadIdx.x >> 5];
+    for (int i = threadIdx.x; i < (int)(sizeof(CostConst) / 8); i += blockDim.x)
+        reinterpret_cast<double *>(&cost)[i] = reinterpret_cast<const double *>(&a.cost)[i];
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31u;
+    const int NC = a.NC;                 // == NCc (dispatch)
+    constexpr int NCc = NC2 ? 2 : 1;
+    uint32_t err = 0u;
+    // Segment pipeline: the next segment's metadata is loaded into registers
+    // and its tokens are prefetched into L2 while the current one streams, so
+    // a short segment costs one L2 round trip instead of several HBM ones.
+    // Queue tickets hand out batches of a.seg_batch segments; lane 0 holds
+    // the ticket of the next batch.
+    struct Pre {
+        int64_t sl, s0, s1;
+        int meta, ml;
+        bool cell_ok;
+        uint32_t T[N > 1 ? N - 1 : 1];
+    };
+    auto load_pre = [&](int64_t sl) {
+        Pre p;
+        p.sl = sl;
+        p.meta = -3;
+        p.s0 = p.s1 = 0;
+        p.ml = 0;
+        p.cell_ok = false;
+#pragma unroll
+        for (int i = 0; i + 1 < N; ++i) p.T[i] = 0xFFFFFFFFu;
+        if (sl < a.n_segments) {
+            p.meta = a.seg_meta[sl];
+            p.s0 = a.seg_offsets[sl];
+            p.s1 = a.seg_offsets[sl + 1];
+            p.cell_ok = a.cell_status[sl] == SPROUT_CELL_OK;
+#pragma unroll
+            for (int i = 0; i + 1 < N; ++i) p.T[i] = a.threshold[sl * (N - 1) + i];
+            p.ml = a.max_level[sl];
+        }
+        return p;
+    };
+    auto prefetch_tokens = [&](const Pre &p) {   // lane l: line l of every plane (<= 2048 requests)
+        if (p.meta < -1 || p.s1 <= p.s0) return;
+        const int64_t b0 = (p.s0 * 2) & ~(int64_t)127, b1 = p.s1 * 2;
+        const int64_t off = b0 + 128 * (int64_t)lane;
+        if (off < b1) {
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint8_t *>(a.tokens + (size_t)i * a.pitch) + off));
+        }
+        if (FLAGS) {
+            const int64_t f0 = p.s0 & ~(int64_t)127, fo = f0 + 128 * (int64_t)lane;
+            if (fo < p.s1) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.flags + fo));
+        }
+    };
+    const int64_t B = a.seg_batch;
+    int64_t it_seg = 0, it_end = 0;
+    uint32_t pend = 0u;
+    if (lane == 0) pend = atomicAdd(a.queue, 1u);
+    auto next_segment = [&]() -> int64_t {
+        if (it_seg >= it_end) {
+            it_seg = (int64_t)__shfl_sync(0xFFFFFFFFu, pend, 0) * B;
+            it_end = min(it_seg + B, a.n_segments);
+            if (it_seg >= a.n_segments) return a.n_segments;
+            if (lane == 0) pend = atomicAdd(a.queue, 1u);
+        }
+        return it_seg++;
+    };
+    Pre cur = load_pre(next_segment());
+    prefetch_tokens(cur);
+    for (;;) {
+        const int64_t sl = cur.sl;
+        if (sl >= a.n_segments) break;
+        const Pre nxt = load_pre(next_segment());
+        const int64_t s = a.first_segment + sl;
+        const int meta = cur.meta;
+        if (meta == -2) {   // invalid offsets (prep): segment skipped, outputs zero
+            err |= SPROUT_TRACE_BAD_OFFSETS;
+            if (lane < (uint32_t)(NC * N)) { a.cnt[sl * NC * N + lane] = 0ull; a.tok[sl * NC * N + lane] = 0ull; }
+            if (lane < (uint32_t)NC) { a.seg_count[sl * NC + lane] = 0ull; a.seg_pinned[sl * NC + lane] = 0ull; }
+            if (lane < (uint32_t)(NC * N)) a.seg_tok[sl * NC * N + lane] = 0ull;
+            if (lane < 4) a.seg_base[sl * 4 + lane] = 0.0;
+            if (lane == 0) { a.energy[sl] = 0.0; a.time_s[sl] = 0.0; a.carbon[sl] = 0.0; a.quality[sl] = 0.0; }
+            cur = nxt;
+            prefetch_tokens(cur);
+            continue;
+        }
+        prefetch_tokens(nxt);
+        const int64_t s0 = cur.s0, s1 = cur.s1;
+        const bool cell_ok = cur.cell_ok;
+        uint32_t T[N > 1 ? N - 1 : 1];
+#pragma unroll
+        for (int i = 0; i + 1 < N; ++i) T[i] = cur.T[i];
+        const int ml = cur.ml;
+
+        constexpr int NCc_N = (NC2 ? 2 : 1) * N;
+        constexpr int oCC = 0, oCT = NCc_N, oST = 2 * NCc_N, oST1 = oST + N, oCV = oST1 + N, oC1 = oCV + 1,
+                      oSP = oC1 + 1;
+        if (lane < (uint32_t)kTot) tot[lane] = 0ull;
+        __syncwarp();
+        for (int64_t c0 = s0; c0 < s1; c0 += kX1Chunk) {
+            const int64_t c1 = min(s1, c0 + kX1Chunk);
+            uint32_t cc[NCc * N], ct[NCc * N], st[N], st1[N], cv = 0, cl1 = 0, sp[NCc];
+#pragma unroll
+            for (int k = 0; k < NCc * N; ++k) { cc[k] = 0; ct[k] = 0; }
+#pragma unroll
+            for (int i = 0; i < N; ++i) { st[i] = 0; st1[i] = 0; }
+#pragma unroll
+            for (int c = 0; c < NCc; ++c) sp[c] = 0;
+            const int64_t gq0 = (int64_t)((a.first_request + (uint64_t)c0) >> 2);   // global quad of c0
+            const int64_t gq1 = (int64_t)((a.first_request + (uint64_t)c1 + 3) >> 2);
+            // quads in pairs (both quads' loads in flight together), L2 prefetch 8 iterations ahead
+            auto quad = [&](int64_t gq, const uint2 (&tw)[N], uint32_t fw, bool valid) {
+                const int64_t r4 = gq * 4 - (int64_t)a.first_request;
+                const Philox4 d = philox4x32_10_rk((uint32_t)gq, (uint32_t)((uint64_t)gq >> 32), 0u, 0u, a.rk0, a.rk1);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int64_t r = r4 + j;
+                    const uint32_t w = d.v[j];
+                    uint32_t cls = 0u, pin = 0u;
+                    if (FLAGS) {
+                        const uint32_t fb = (fw >> (8 * j)) & 0xFFu;
+                        pin = fb & 1u;
+                        cls = (fb >> 1) & 3u;
+                    }
+                    const bool inr = valid && r >= c0 && r < c1;
+                    const bool okc = cls < (uint32_t)NC;
+                    if (inr && !okc) err |= SPROUT_TRACE_BAD_CLASS;
+                    const bool ok = inr && okc;
+                    int L = 0;
+#pragma unroll
+                    for (int i = 0; i + 1 < N; ++i) L += (w >= T[i]) ? 1 : 0;
+                    L = min(L, ml);
+                    L = pin ? 0 : L;
+                    uint32_t t[N], tL = 0u;
+#pragma unroll
+                    for (int i = 0; i < N; ++i) {
+                        const uint32_t word = (j >> 1) ? tw[i].y : tw[i].x;
+                        t[i] = (j & 1) ? (word >> 16) : (word & 0xFFFFu);
+                        tL = (L == i) ? t[i] : tL;
+                    }
+                    const bool is1 = NC2 && cls == 1u;
+                    cv += ok ? 1u : 0u;
+                    cl1 += (ok && is1) ? 1u : 0u;
+#pragma unroll
+                    for (int c = 0; c < NCc; ++c) sp[c] += (ok && pin && (int)cls == c) ? 1u : 0u;
+#pragma unroll
+                    for (int i = 0; i < N; ++i) {
+                        st[i] += ok ? t[i] : 0u;
+                        if (NC2) st1[i] += (ok && is1) ? t[i] : 0u;
+                    }
+                    const int idx = L + (is1 ? N : 0);
+#pragma unroll
+                    for (int k = 0; k < NCc * N; ++k) {
+                        const bool hit = ok && idx == k;
+                        cc[k] += hit ? 1u : 0u;
+                        ct[k] += hit ? tL : 0u;
+                    }
+                }
+            };
+            auto load = [&](int64_t gq, uint2 (&tw)[N], uint32_t &fw) {
+                const int64_t r4 = gq * 4 - (int64_t)a.first_request;
+#pragma unroll
+                for (int i = 0; i < N; ++i)
+                    tw[i] = __ldcs(reinterpret_cast<const uint2 *>(a.tokens + (size_t)i * a.pitch + r4));
+                fw = FLAGS ? __ldcs(reinterpret_cast<const uint32_t *>(a.flags + r4)) : 0u;
+                const int64_t rp = r4 + 4 * 32 * 8;
+                if (rp < c1) {
+#pragma unroll
+                    for (int i = 0; i < N; ++i)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(a.tokens + (size_t)i * a.pitch + rp));
+                }
+            };
+            for (int64_t gq = gq0 + lane; gq < gq1; gq += 32) {
+                uint2 ta[N];
+                uint32_t fa;
+                load(gq, ta, fa);
+                quad(gq, ta, fa, true);
+            }
+            // fold the chunk into the warp's 64-bit totals
+            auto fold = [&](int o, uint32_t v) {
+                const uint32_t sum = __reduce_add_sync(0xFFFFFFFFu, v);
+                if (lane == 0) tot[o] += sum;
+            };
+#pragma unroll
+            for (int k = 0; k < NCc * N; ++k) { fold(oCC + k, cc[k]); fold(oCT + k, ct[k]); }
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                fold(oST + i, st[i]);
+                if (NC2) fold(oST1 + i, st1[i]);
+            }
+            fold(oCV, cv);
+            if (NC2) fold(oC1, cl1);
+#pragma unroll
+            for (int c = 0; c < NCc; ++c) fold(oSP + c, sp[c]);
+        }
+        __syncwarp();
+
+        // per-class segment statistics and the Base counterfactual (write_seg_stats' order)
+        const int64_t qrow_i = a.profile_per_interval ? s
+                             : (s < 0xFFFFFFFFll ? (int64_t)a.div_t.div((uint32_t)s) : s / a.T);
+        const double *qrow = a.q + qrow_i * N;
+        const double kp = a.k0[s] * a.pue;
+        if (lane == 0) {
+            const unsigned long long c1n = NC2 ? tot[oC1] : 0ull;
+            double bE = 0.0, bT = 0.0, m = 0.0;
+#pragma unroll
+            for (int c = 0; c < NCc; ++c) {
+                const unsigned long long mc = c == 0 ? tot[oCV] - c1n : c1n;
+                a.seg_count[sl * NCc + c] = mc;
+                a.seg_pinned[sl * NCc + c] = tot[oSP + c];
+                unsigned long long t0 = 0ull;
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                    const unsigned long long t1 = NC2 ? tot[oST1 + i] : 0ull;
+                    const unsigned long long tc = c == 0 ? tot[oST + i] - t1 : t1;
+                    a.seg_tok[(sl * NCc + c) * N + i] = tc;
+                    if (i == 0) t0 = tc;
+                }
+                bE += (double)mc * cost.ef[c][0] + (double)t0 * cost.et[c][0];
+                bT += (double)mc * cost.pf[c][0] + (double)t0 * cost.pt[c][0];
+                m += (double)mc;
+            }
+            a.seg_base[sl * 4 + 0] = bE;
+            a.seg_base[sl * 4 + 1] = bT;
+            a.seg_base[sl * 4 + 2] = kp * bE + a.k1 * bT;
+            a.seg_base[sl * 4 + 3] = m * qrow[0];
+            // the cell (cell_epilogue's order)
+            double E = 0.0, Tm = 0.0, Q = 0.0;
+#pragma unroll
+            for (int c = 0; c < NCc; ++c) {
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    const unsigned long long cn = cell_ok ? tot[oCC + c * N + L] : 0ull;
+                    const unsigned long long tk = cell_ok ? tot[oCT + c * N + L] : 0ull;
+                    a.cnt[(sl * NCc + c) * N + L] = cn;
+                    a.tok[(sl * NCc + c) * N + L] = tk;
+                    const double n_ = (double)cn, t_ = (double)tk;
+                    E += n_ * cost.ef[c][L] + t_ * cost.et[c][L];
+                    Tm += n_ * cost.pf[c][L] + t_ * cost.pt[c][L];
+                    Q += n_ * qrow[L];
+                }
+            }
+            a.energy[sl] = E;
+            a.time_s[sl] = Tm;
+            a.carbon[sl] = cell_ok ? kp * E + a.k1 * Tm : 0.0;
+            a.quality[sl] = Q;
+        }
+        __syncwarp();
+        cur = nxt;
+    }
+    err = __reduce_or_sync(0xFFFFFFFFu, err);
+    if (lane == 0 && err) atomicOr(a.trace_status, err);
+}
+
+template <int N, bool FLAGS, bool NC2>
+static cudaError_t launch_x1_t(SimArgs &a, cudaStream_t stream) {
+    auto kern = trace_x1_kernel<N, FLAGS, NC2>;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * kX1Warps, 0);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    const int64_t warps = (int64_t)sms * per_sm * kX1Warps;
+    int64_t bsz = a.n_segments / (warps * 16);
+    a.seg_batch = (int)(bsz < 1 ? 1 : (bsz > 16 ? 16 : bsz));
+    int64_t grid = (int64_t)sms * per_sm;
+    const int64_t need = (a.n_segments + kX1Warps - 1) / kX1Warps;
+    if (grid > need) grid = need > 0 ? need : 1;
+    kern<<<(unsigned)grid, 32 * kX1Warps, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+bool trace_x1_supported(int n, int X, int NC) { return X == 1 && n >= 1 && n <= 4 && NC >= 1 && NC <= 2; }
+
+cudaError_t launch_trace_x1(SimArgs &a, cudaStream_t stream) {
+    const bool fl = a.flags != nullptr, nc2 = a.NC == 2;
+#define X1_CASE(NN)                                                                                      \
+    case NN:                                                                                             \
+        return fl ? (nc2 ? launch_x1_t<NN, true, true>(a, stream) : launch_x1_t<NN, true, false>(a, stream)) \
+                  : (nc2 ? launch_x1_t<NN, false, true>(a, stream) : launch_x1_t<NN, false, false>(a, stream));
+    switch (a.n) {
+        X1_CASE(1) X1_CASE(2) X1_CASE(3) X1_CASE(4)
+        default: return cudaErrorInvalidValue;
+    }
+#undef X1_CASE
+}
+
+}  // namespace sprout

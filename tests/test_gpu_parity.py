@@ -362,3 +362,69 @@ def test_c4_full_size_sampled():
     G = got["group"]
     assert G[-1, 0, 0] == 10**9
     np.testing.assert_array_equal(G[-1, :, 11:14].sum(axis=1), G[-1, :, 0])
+
+
+# ---------------------------------------------------------------- one cell per segment (trace_x1.cu)
+
+
+@pytest.mark.parametrize("n,NC,flags", [(1, 1, False), (2, 2, True), (3, 1, True), (3, 2, False), (4, 2, True),
+                                        (4, 1, False)])
+def test_x1_register_path(n, NC, flags):
+    """X = 1, n <= 4, <= 2 classes: the register path; ragged and empty
+    segments, a long segment and tokens >= 4096 included."""
+    w = _custom(n=n, X=1, NC=NC, flags=flags, N=40_000, T=40, R=2, xi=[0.3])
+    off = w.spec.seg_offsets
+    m = np.diff(off)
+    m[::7] = 0
+    m[3] = 1
+    m[5] = 3
+    m[9] = 9000
+    off[1:] = np.cumsum(m)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, fl = synth.host_trace(w.spec, sh)
+    rng = np.random.default_rng(n)
+    idx = rng.integers(0, sh.n_requests, 300)
+    toks[rng.integers(0, n, 300), idx] = rng.integers(4096, 65536, 300)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=fl)
+    sw.step()
+    sw.simulate(levels=True)
+    torch.cuda.synchronize()
+    got = sw.host()
+    cells = oracle.solve_cells(w.prob)
+    compare_cells(got, cells)
+    sim = oracle_shard(w, sh, toks, fl, levels=True)
+    compare_sim(got, sim, 1, NC, n)
+    np.testing.assert_array_equal(got["levels"][:, :sh.n_requests], sim["levels"][:, :sh.n_requests])
+    G = oracle.reduce(w.prob, NC, 0, w.prob.R * w.prob.T, cells, sim)
+    np.testing.assert_allclose(got["group"], G, rtol=FP_RTOL, atol=1e-300)
+
+
+def test_x1_bad_class_invalid_cell_bad_offsets():
+    w = _custom(N=6000, T=8, R=1, NC=2, flags=True, X=1, xi=[0.2])
+    sh = synth.shard(w.spec, 1, 0)
+    toks, flags = synth.host_trace(w.spec, sh)
+    flags[sh.seg_offsets[2] + 1] = 3 << 1             # class 3 >= n_classes: skipped, flagged
+    w.prob.k0 = w.prob.k0.copy()
+    w.prob.k0[4] = -1.0                               # invalid cell: totals 0, segment stats still counted
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=flags)
+    sw.step()
+    torch.cuda.synchronize()
+    got = sw.host()
+    assert got["trace_status"] & S.TRACE_BAD_CLASS
+    assert got["cell_status"][4] == S.CELL_INVALID
+    sim = oracle_shard(w, sh, toks, flags)
+    assert sim["bad_requests"] == 1
+    compare_sim(got, sim, 1, 2, 3)
+    bad = sw.trace.seg_offsets.clone(); bad[3] = bad[4] + 1
+    sw.trace.seg_offsets = bad
+    sw.simulate()
+    torch.cuda.synchronize()
+    got = sw.host()
+    assert got["trace_status"] & S.TRACE_BAD_OFFSETS
+    assert got["seg_count"].reshape(-1, 2)[3].sum() == 0
+
+
+def test_x1_long_segment_folds():
+    # 5M requests in one segment: three 2^21-request folds of the 32-bit lane sums
+    w = _custom(N=5_000_000, T=1, R=1, X=1, xi=[0.5])
+    check_full(w, levels=False)
