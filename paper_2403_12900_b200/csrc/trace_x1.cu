@@ -1,6 +1,6 @@
 // trace_x1.cu -- step 2 of the hot path for ONE cell per segment (X = 1:
-// configs C1 and C3, and any single-xi sweep) with n <= 4 levels and <= 2
-// model classes.  With a single cell the level of a request is the a6 rule
+// configs C1, C3 and C5, and any single-xi sweep) with n <= 4 levels and
+// <= 2 model classes, or n <= 8 levels and one class.  With a single cell the level of a request is the a6 rule
 // itself -- level = pinned ? 0 : min(#{i : w >= T_i}, max_level) (P:162,
 // P:240; reading L10) -- so no breakpoint merge or histogram is needed: a
 // warp owns a segment, each lane takes aligned quads of 4 consecutive
@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(32 * kX1Warps, 3) trace_x1_kernel(const __grid
     // per-warp 64-bit totals of a segment: [0, NC*N) cell counts, [NC*N, 2NC*N) cell tokens,
     // then tokens per level (all classes), class-1 tokens per level, valid requests,
     // class-1 requests, pinned per class
-    constexpr int kTot = 4 * 4 + 2 * 4 + 2 + 2;
+    constexpr int kTot = 2 * (NC2 ? 2 : 1) * N + 2 * N + 2 + 2;   // <= 36 (N <= 4 with 2 classes, N <= 8 with 1)
     __shared__ unsigned long long tot_s[kX1Warps][kTot];
     unsigned long long *tot = tot_s[threadIdx.x >> 5];
     for (int i = threadIdx.x; i < (int)(sizeof(CostConst) / 8); i += blockDim.x)
@@ -121,11 +121,14 @@ __global__ void __launch_bounds__(32 * kX1Warps, 3) trace_x1_kernel(const __grid
 #pragma unroll
         for (int i = 0; i + 1 < N; ++i) T[i] = cur.T[i];
         const int ml = cur.ml;
+        bool pure = true;
+#pragma unroll
+        for (int i = 0; i + 1 < N; ++i) pure = pure && (T[i] == 0u || T[i] == 0xFFFFFFFFu);
 
         constexpr int NCc_N = (NC2 ? 2 : 1) * N;
         constexpr int oCC = 0, oCT = NCc_N, oST = 2 * NCc_N, oST1 = oST + N, oCV = oST1 + N, oC1 = oCV + 1,
                       oSP = oC1 + 1;
-        if (lane < (uint32_t)kTot) tot[lane] = 0ull;
+        for (int i = lane; i < kTot; i += 32) tot[i] = 0ull;
         __syncwarp();
         for (int64_t c0 = s0; c0 < s1; c0 += kX1Chunk) {
             const int64_t c1 = min(s1, c0 + kX1Chunk);
@@ -141,7 +144,15 @@ __global__ void __launch_bounds__(32 * kX1Warps, 3) trace_x1_kernel(const __grid
             // quads in pairs (both quads' loads in flight together), L2 prefetch 8 iterations ahead
             auto quad = [&](int64_t gq, const uint2 (&tw)[N], uint32_t fw, bool valid) {
                 const int64_t r4 = gq * 4 - (int64_t)a.first_request;
-                const Philox4 d = philox4x32_10_rk((uint32_t)gq, (uint32_t)((uint64_t)gq >> 32), 0u, 0u, a.rk0, a.rk1);
+                // a pure mix (every threshold 0 or saturated) selects the same level for every
+                // draw: no draw is needed (warp-uniform)
+                Philox4 d;
+                if (pure) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) d.v[j] = 0u;
+                } else {
+                    d = philox4x32_10_rk((uint32_t)gq, (uint32_t)((uint64_t)gq >> 32), 0u, 0u, a.rk0, a.rk1);
+                }
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int64_t r = r4 + j;
@@ -301,7 +312,9 @@ static cudaError_t launch_x1_t(SimArgs &a, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-bool trace_x1_supported(int n, int X, int NC) { return X == 1 && n >= 1 && n <= 4 && NC >= 1 && NC <= 2; }
+bool trace_x1_supported(int n, int X, int NC) {
+    return X == 1 && n >= 1 && ((NC == 2 && n <= 4) || (NC == 1 && n <= 8));
+}
 
 cudaError_t launch_trace_x1(SimArgs &a, cudaStream_t stream) {
     const bool fl = a.flags != nullptr, nc2 = a.NC == 2;
@@ -309,10 +322,15 @@ cudaError_t launch_trace_x1(SimArgs &a, cudaStream_t stream) {
     case NN:                                                                                             \
         return fl ? (nc2 ? launch_x1_t<NN, true, true>(a, stream) : launch_x1_t<NN, true, false>(a, stream)) \
                   : (nc2 ? launch_x1_t<NN, false, true>(a, stream) : launch_x1_t<NN, false, false>(a, stream));
+#define X1_CASE1(NN)                                                                                     \
+    case NN:                                                                                             \
+        return fl ? launch_x1_t<NN, true, false>(a, stream) : launch_x1_t<NN, false, false>(a, stream);
+    if (nc2 && a.n > 4) return cudaErrorInvalidValue;
     switch (a.n) {
-        X1_CASE(1) X1_CASE(2) X1_CASE(3) X1_CASE(4)
+        X1_CASE(1) X1_CASE(2) X1_CASE(3) X1_CASE(4) X1_CASE1(5) X1_CASE1(6) X1_CASE1(7) X1_CASE1(8)
         default: return cudaErrorInvalidValue;
     }
+#undef X1_CASE1
 #undef X1_CASE
 }
 

@@ -368,10 +368,10 @@ def test_c4_full_size_sampled():
 
 
 @pytest.mark.parametrize("n,NC,flags", [(1, 1, False), (2, 2, True), (3, 1, True), (3, 2, False), (4, 2, True),
-                                        (4, 1, False)])
+                                        (4, 1, False), (5, 1, False), (6, 1, True), (8, 1, False)])
 def test_x1_register_path(n, NC, flags):
-    """X = 1, n <= 4, <= 2 classes: the register path; ragged and empty
-    segments, a long segment and tokens >= 4096 included."""
+    """X = 1 (n <= 4 with <= 2 classes, n <= 8 with one): the register path;
+    ragged and empty segments, a long segment and tokens >= 4096 included."""
     w = _custom(n=n, X=1, NC=NC, flags=flags, N=40_000, T=40, R=2, xi=[0.3])
     off = w.spec.seg_offsets
     m = np.diff(off)
@@ -428,3 +428,10 @@ def test_x1_long_segment_folds():
     # 5M requests in one segment: three 2^21-request folds of the 32-bit lane sums
     w = _custom(N=5_000_000, T=1, R=1, X=1, xi=[0.5])
     check_full(w, levels=False)
+
+
+@pytest.mark.parametrize("xi", [0.0, 1.0])
+def test_x1_pure_mix_skips_draws(xi):
+    # xi = 0: pure L0 (no draw needed); xi = 1 at high intensity: a pure or an edge mix per segment
+    w = _custom(n=5, X=1, N=60_000, T=30, R=2, xi=[xi])
+    check_full(w)
