@@ -68,18 +68,20 @@ __global__ void __launch_bounds__(32 * kX1Warps, 3) trace_x1_kernel(const __grid
         }
         return p;
     };
-    auto prefetch_tokens = [&](const Pre &p) {   // lane l: line l of every plane (<= 2048 requests)
+    // lanes 0..7: the first 8 lines (512 requests) of every plane -- a whole short segment; a long
+    // one is prefetched inside its loop (more would evict lines from L2 before they are used)
+    auto prefetch_tokens = [&](const Pre &p) {
         if (p.meta < -1 || p.s1 <= p.s0) return;
         const int64_t b0 = (p.s0 * 2) & ~(int64_t)127, b1 = p.s1 * 2;
         const int64_t off = b0 + 128 * (int64_t)lane;
-        if (off < b1) {
+        if (lane < 8 && off < b1) {
 #pragma unroll
             for (int i = 0; i < N; ++i)
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint8_t *>(a.tokens + (size_t)i * a.pitch) + off));
         }
         if (FLAGS) {
             const int64_t f0 = p.s0 & ~(int64_t)127, fo = f0 + 128 * (int64_t)lane;
-            if (fo < p.s1) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.flags + fo));
+            if (lane < 4 && fo < p.s1) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.flags + fo));
         }
     };
     const int64_t B = a.seg_batch;
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(32 * kX1Warps, 3) trace_x1_kernel(const __grid
                         pin = fb & 1u;
                         cls = (fb >> 1) & 3u;
                     }
-                    const bool inr = valid && r >= c0 && r < c1;
+                    const bool inr = valid && (uint64_t)(r - c0) < (uint64_t)(c1 - c0);
                     const bool okc = cls < (uint32_t)NC;
                     if (inr && !okc) err |= SPROUT_TRACE_BAD_CLASS;
                     const bool ok = inr && okc;
