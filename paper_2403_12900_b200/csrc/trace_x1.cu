@@ -213,11 +213,59 @@ __global__ void __launch_bounds__(32 * kX1Warps, 3) trace_x1_kernel(const __grid
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(a.tokens + (size_t)i * a.pitch + rp));
                 }
             };
-            for (int64_t gq = gq0 + lane; gq < gq1; gq += 32) {
-                uint2 ta[N];
-                uint32_t fa;
-                load(gq, ta, fa);
-                quad(gq, ta, fa, true);
+            if (!FLAGS && !NC2 && pure) {
+                // pure mix, no flags: every request is at the same level -- a streaming sum of the
+                // token planes (interior quads whole, the two edge quads per request)
+                int Lp = 0;
+#pragma unroll
+                for (int i = 0; i + 1 < N; ++i) Lp += (T[i] == 0u) ? 1 : 0;
+                Lp = min(Lp, ml);
+                constexpr int U = N <= 3 ? 4 : 2;   // quads in flight per lane (registers)
+                for (int64_t base = gq0 + lane; base < gq1; base += 32 * U) {
+                    uint2 ta[U][N];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        uint32_t fa;
+                        load(min(base + 32 * u, gq1 - 1), ta[u], fa);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int64_t gq = base + 32 * u;
+                        if (gq >= gq1) break;
+                        const int64_t r4 = gq * 4 - (int64_t)a.first_request;
+                        if (r4 >= c0 && r4 + 4 <= c1) {
+#pragma unroll
+                            for (int i = 0; i < N; ++i)
+                                st[i] += (ta[u][i].x & 0xFFFFu) + (ta[u][i].x >> 16) + (ta[u][i].y & 0xFFFFu) +
+                                         (ta[u][i].y >> 16);
+                            cv += 4u;
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                if ((uint64_t)(r4 + j - c0) < (uint64_t)(c1 - c0)) {
+#pragma unroll
+                                    for (int i = 0; i < N; ++i) {
+                                        const uint32_t word = (j >> 1) ? ta[u][i].y : ta[u][i].x;
+                                        st[i] += (j & 1) ? (word >> 16) : (word & 0xFFFFu);
+                                    }
+                                    cv += 1u;
+                                }
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                    cc[i] = (i == Lp) ? cv : 0u;
+                    ct[i] = (i == Lp) ? st[i] : 0u;
+                }
+            } else {
+                for (int64_t gq = gq0 + lane; gq < gq1; gq += 32) {
+                    uint2 ta[N];
+                    uint32_t fa;
+                    load(gq, ta, fa);
+                    quad(gq, ta, fa, true);
+                }
             }
             // fold the chunk into the warp's 64-bit totals
             auto fold = [&](int o, uint32_t v) {
