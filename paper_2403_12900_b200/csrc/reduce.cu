@@ -17,7 +17,10 @@
 namespace sprout {
 
 constexpr int kRedThreads = 256;
-constexpr int kRedPerThread = 16;   // intervals per thread per chunk
+#ifndef SPROUT_RED_PER_THREAD
+#define SPROUT_RED_PER_THREAD 16
+#endif
+constexpr int kRedPerThread = SPROUT_RED_PER_THREAD;   // intervals per thread per chunk
 
 // column tile width (power of two >= X, <= 256) and interval phases per block
 static inline __host__ __device__ int red_xp(int X) {
