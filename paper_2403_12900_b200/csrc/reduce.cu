@@ -18,7 +18,7 @@ namespace sprout {
 
 constexpr int kRedThreads = 256;
 #ifndef SPROUT_RED_PER_THREAD
-#define SPROUT_RED_PER_THREAD 16
+#define SPROUT_RED_PER_THREAD 4
 #endif
 constexpr int kRedPerThread = SPROUT_RED_PER_THREAD;   // intervals per thread per chunk
 
