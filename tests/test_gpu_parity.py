@@ -333,35 +333,42 @@ def test_sweep_host_matches_device_path():
 
 
 @pytest.mark.slow
-def test_c4_full_size_sampled():
-    """BASELINE config C4 at full size (10^9 requests, generated on the GPU
-    in the bench's launch configuration); the oracle replays a deterministic
-    sample of segments (every 997th + first/last/largest) regenerated on the
-    host from global request indices."""
-    w = synth.make_workload("C4")
+@pytest.mark.parametrize("name,every", [("C4", 997), ("C3", 4999), ("C5", 99991)])
+def test_full_size_sampled(name, every):
+    """BASELINE configs at full size, generated on the GPU in the bench's
+    launch configuration (C4: 10^9 requests, the histogram kernel; C3: 10^8
+    requests in 525,600 five-minute segments with two classes and opted-out
+    users, and C5: 10^10 requests, 256 regions, n = 5 -- both the one-cell
+    kernel); the oracle replays a deterministic sample of segments
+    (every k-th + first/last/largest) regenerated on the host from global
+    request indices."""
+    w = synth.make_workload(name)
     sh = synth.shard(w.spec, 1, 0)
     sw = Sweep(w.prob, w.cost, sh, DEV, spec=w.spec)
     sw.step()
     torch.cuda.synchronize()
     got = sw.host()
     assert got["trace_status"] == 0
+    ids = synth.sample_segments(w.spec, 0, sh.n_segments, every=every)
+    X = w.prob.X
     cells = oracle.solve_cells(w.prob)
     compare_cells(got, cells)
-    ids = synth.sample_segments(w.spec, 0, sh.n_segments, every=997)
     # regenerate only the sampled segments' requests on the host
-    parts, begins, ms, g0s = [], [], [], []
+    parts, fparts, begins, ms, g0s = [], [], [], [], []
     pos = 0
     for s in ids:
         a, b = int(w.spec.seg_offsets[s]), int(w.spec.seg_offsets[s + 1])
-        t, _ = synth.gen_tokens(w.spec, a, b)
-        parts.append(t); begins.append(pos); ms.append(b - a); g0s.append(a); pos += b - a
+        t, f = synth.gen_tokens(w.spec, a, b)
+        parts.append(t); fparts.append(f); begins.append(pos); ms.append(b - a); g0s.append(a); pos += b - a
     toks = np.concatenate(parts, axis=1)
-    sim = oracle.simulate(w.prob, w.cost, ids, np.array(begins), np.array(ms), np.array(g0s, np.uint64), toks, None)
-    compare_sim(got, sim, w.prob.X, 1, 3, loc=ids)
+    flags = np.concatenate(fparts) if w.spec.has_flags else None
+    sim = oracle.simulate(w.prob, w.cost, ids, np.array(begins), np.array(ms), np.array(g0s, np.uint64), toks, flags)
+    compare_sim(got, sim, X, w.cost.n_classes, w.prob.n, loc=ids)
     # conservation on the full run
     G = got["group"]
-    assert G[-1, 0, 0] == 10**9
-    np.testing.assert_array_equal(G[-1, :, 11:14].sum(axis=1), G[-1, :, 0])
+    n = w.prob.n
+    assert G[-1, 0, 0] == w.N
+    np.testing.assert_array_equal(G[-1, :, 11:11 + n].sum(axis=1), G[-1, :, 0])
 
 
 # ---------------------------------------------------------------- one cell per segment (trace_x1.cu)
