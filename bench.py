@@ -299,7 +299,10 @@ def run_sprout(args):
         sw.solve(); launches[0] += S.last_launch_count()
         if ev is not None:
             ev[0].record(stream)
-        sw.simulate(); launches[0] += S.last_launch_count()
+        if args.closed_loop:
+            sw.closed_loop(args.closed_loop); launches[0] += S.last_launch_count()
+        else:
+            sw.simulate(); launches[0] += S.last_launch_count()
         if ev is not None:
             ev[1].record(stream)
         sw.reduce(); launches[0] += S.last_launch_count()
@@ -351,7 +354,7 @@ def run_sprout(args):
 
     # e2e: the host-buffer C-ABI call (H2D of the trace + D2H of the totals timed)
     e2e = None
-    if not args.no_e2e and scheme == S.SCHEME_SPROUT:
+    if not args.no_e2e and scheme == S.SCHEME_SPROUT and not args.closed_loop:
         e2e = run_e2e(args, w, sh, sw, dev, world)
 
     if rank != 0:
@@ -361,6 +364,11 @@ def run_sprout(args):
 
     peak, peak_src = peaks()
     alg = algorithmic_bytes(w, sh)
+    if args.closed_loop:   # each (region, xi) chain reads its requests' selected-level token (+ flags)
+        P = w.prob
+        f = 1 if w.spec.has_flags else 0
+        alg = int(sh.seg_offsets[-1] - sh.seg_offsets[0]) * P.X * (2 + f) + \
+            sh.n_segments * P.X * (P.n * 8 + 8 + 8 + 4 * (P.n - 1) + 3 + w.cost.n_classes * P.n * 16 + 32)
     sim_avg_ms = statistics.mean(sim_ms)
     achieved = alg / (sim_avg_ms * 1e-3) / 1e9
     traffic = None
@@ -370,14 +378,16 @@ def run_sprout(args):
         if d.get("workload") == w.name and d.get("n_gpus", 1) == world:
             traffic = d.get("dram_bytes_per_launch")
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and not args.closed_loop:
         cpu = oracle_baseline(w, args.cpu_seconds, scheme, args.grid_den)
     N = w.N
     line = {
         "metric": METRIC, "value": N / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64/u32", "data": "synthetic",
-        "config": {"workload": workload_desc(w, args.scheme), "config": w.name, "scheme": args.scheme, "requests": N,
+        "config": {"workload": workload_desc(w, args.scheme) + (f" [closed loop, window {args.closed_loop}]"
+                                                                   if args.closed_loop else ""),
+                   "config": w.name, "scheme": args.scheme, "closed_loop_window": args.closed_loop, "requests": N,
                    "lp_cells": w.prob.C,
                    "parallelism": f"segments sharded over {world} GPU(s), one NCCL allreduce of group totals",
                    "l2": ("flushed (256 MB memset) between steps" if flush else
@@ -385,7 +395,8 @@ def run_sprout(args):
         "lp_cells_per_s": w.prob.C / (lp_ms * 1e-3),
         "request_cells_per_s": N * w.prob.X / (ms_per_step * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "sprout_simulate_trace (prep + trace_kernel, CUDA events)",
+                     "traffic": traffic, "kernel": ("sprout_simulate_closed_loop (one CTA per chain)" if args.closed_loop
+                                                    else "sprout_simulate_trace (prep + trace_kernel, CUDA events)"),
                      "algorithmic_bytes_per_launch": alg, "launch_ms": sim_avg_ms, "peak_source": peak_src},
         "clocks": clk.summary(),
         "gpu_launches": launches[0],
@@ -473,6 +484,8 @@ def main():
                     help="competing scheme of P:364-373 (co2opt, static = the Sprout_Sta grid sweep)")
     ap.add_argument("--grid-den", type=int, default=20, help="static grid step 1/D (Sprout_Sta sweep)")
     ap.add_argument("--static-xi", type=float, default=0.1, help="xi of the Sprout_Sta quality floor")
+    ap.add_argument("--closed-loop", type=int, default=0, metavar="W",
+                    help="closed-loop profiles (NEXT-1): window of W requests per level; 0 = open loop")
     ap.add_argument("--evaluator", action="store_true",
                     help="time the opportunistic evaluator trigger sweep (Eq. 8) instead of the hot path")
     args = ap.parse_args()

@@ -16,7 +16,7 @@
  *   3. sprout_reduce_totals: per (region, xi) and per xi group totals; the
  *      caller then all-reduces them across GPUs (NCCL, torch.distributed).
  * P:<line> cites /root/reference/PAPER.md.  Readings of silent or ambiguous
- * passages (tie-break, rounding order, RNG layout, ...) are DESIGN.md L1-L18.
+ * passages (tie-break, rounding order, RNG layout, ...) are DESIGN.md L1-L20.
  *
  * Conventions
  *   - Every array pointer inside the structs is a DEVICE pointer (cudaMalloc
@@ -342,6 +342,34 @@ typedef struct {
  * CUDA.  One thread per configuration; deterministic. */
 sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *problem, double *out,
                                      sprout_stream stream);
+
+/* ---------------------------------------------------------------------- */
+/* Closed-loop profiles (reading L20).  P:183: e and p
+ * are "the average energy consumption and processing time for recent
+ * requests at each level".  Steps 1-2 as one causal scan per (region, xi)
+ * chain: at interval t the profile of level L is the mean Eq. 1 energy and
+ * time of the last `window` requests this chain ran at level L (any class;
+ * opted-out requests count at L0), or the problem's e/p[r][L] (priors) while
+ * none has; with E = ef + et*tok it is computed from the window's per-class
+ * request counts n_c and token sums k_c (exact integers) as
+ *   e_L = (sum_c (n_c ef[c][L] + k_c et[c][L])) / sum_c n_c   (class order),
+ * p_L likewise.  The interval's LP (as sprout_solve_directives) uses it; the
+ * interval's requests are then selected and accounted exactly as in
+ * sprout_simulate_trace, and pushed in request order into their level's
+ * window.  Writes every field of `solution` and the per-cell fields of
+ * `totals` (cnt, tok, energy_kwh, time_s, carbon_g, quality, trace_status;
+ * the segment fields are not written -- they do not depend on the scheme,
+ * sprout_simulate_trace gives them).  `profile_out` is NULL or (device)
+ * [cells][2][n]: the e and p each interval's LP used.  One CTA per chain;
+ * sequential in t by definition.  Requires the whole problem on this device
+ * (first_segment 0, n_segments R*T), profile_per_interval 0, and
+ * 1 <= window <= 4096 with n*window*4 bytes <= 192 KiB.  Errors:
+ * INVALID_ARGUMENT (as sprout_simulate_trace, plus the above); CUDA. */
+sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int32_t window,
+                                          const sprout_trace *trace, const sprout_cost_model *cost,
+                                          const sprout_lp_solution *solution,
+                                          const sprout_cell_totals *totals, double *profile_out,
+                                          sprout_stream stream);
 
 /* Number of kernel launches (not memsets) the last successful call of each
  * entry point on this thread enqueued -- for launch accounting in benches. */

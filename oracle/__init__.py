@@ -103,6 +103,11 @@ def _bind(L):
     L.orc_evaluator_sweep.argtypes = [C.c_int, C.c_int64, C.c_double, _dp, _dp, C.c_int, _dp, C.c_int, _dp,
                                       C.c_double, C.c_int, C.c_double, C.c_double, _dp]
     L.orc_evaluator_sweep.restype = C.c_int
+    L.orc_closed_loop.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                  C.c_double, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp, _dp, C.c_int,
+                                  _i64p, _u16p, C.c_int64, _u8p, _dp, _u64p, _u8p, _dp, _u64p, _u64p, _dp, _dp, _dp,
+                                  _dp]
+    L.orc_closed_loop.restype = C.c_int
     return L
 
 
@@ -318,4 +323,35 @@ def evaluator_sweep(k2, k2max, T: int, dt: float, betas, thetas, grace: float, f
                                    float(pue), _p(out, _dp))
     if st != 0:
         raise ValueError("oracle evaluator_sweep: invalid argument")
+    return out
+
+
+def closed_loop(prob, cost, window: int, seg_offsets, tokens, flags=None):
+    """Closed-loop profiles (NEXT-1): per (region, xi) chain, the LP of
+    each interval uses the mean E and T of the last `window` requests run at
+    each level.  Requests are global: tokens [n][pitch] indexed by the global
+    request index, seg_offsets [R*T+1] global."""
+    n, R, T, X, NC = prob.n, prob.R, prob.T, prob.X, cost.n_classes
+    assert not prob.profile_per_interval
+    tokens = np.ascontiguousarray(tokens, dtype=np.uint16)
+    off = np.ascontiguousarray(seg_offsets, dtype=np.int64)
+    fl = None if flags is None else np.ascontiguousarray(flags, dtype=np.uint8)
+    cells = R * T * X
+    out = dict(x=np.zeros((cells, n)), threshold=np.zeros((cells, max(n - 1, 1)), np.uint64),
+               cell_status=np.zeros(cells, np.uint8), profile=np.zeros((cells, 2, n)),
+               cnt=np.zeros((cells, NC, n), np.uint64),
+               tok=np.zeros((cells, NC, n), np.uint64), energy=np.zeros(cells), time=np.zeros(cells),
+               carbon=np.zeros(cells), quality=np.zeros(cells))
+    ef = _f64(cost.ef); et = _f64(cost.et); pf = _f64(cost.pf); pt = _f64(cost.pt)
+    st = lib().orc_closed_loop(n, R, int(T), X, _p(_f64(prob.k0), _dp), _p(_f64(prob.kmin), _dp),
+                               _p(_f64(prob.kmax), _dp), _p(_f64(prob.xi), _dp), _p(_f64(prob.e), _dp),
+                               _p(_f64(prob.p), _dp), _p(_f64(prob.q), _dp), float(prob.k1), float(prob.pue),
+                               C.c_uint64(int(cost.seed)), NC, _p(ef, _dp), _p(et, _dp), _p(pf, _dp), _p(pt, _dp),
+                               int(window), _p(off, _i64p), _p(tokens, _u16p), tokens.shape[1], _p(fl, _u8p),
+                               _p(out["x"], _dp), _p(out["threshold"], _u64p), _p(out["cell_status"], _u8p),
+                               _p(out["profile"], _dp), _p(out["cnt"], _u64p), _p(out["tok"], _u64p), _p(out["energy"], _dp),
+                               _p(out["time"], _dp), _p(out["carbon"], _dp), _p(out["quality"], _dp))
+    if st != 0:
+        raise ValueError("oracle closed_loop: invalid argument")
+    out["threshold"] = out["threshold"][:, : n - 1]
     return out

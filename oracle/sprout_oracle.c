@@ -765,3 +765,111 @@ int orc_evaluator_sweep(int R, int64_t T, double dt, const double *k2, const dou
             }
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Closed-loop profiles (reading L20).  P:183: the
+ * optimiser's e and p are "the average energy consumption and processing
+ * time for recent requests at each level".  Per (region r, xi_j) chain, in
+ * interval order: the profile of level L is the mean of Eq. 1's E and T
+ * over the last W requests executed at level L (by this chain, any class;
+ * pinned requests count at L0), or the caller's prior e/p[r][L] while none
+ * has run.  With E = ef[c][L] + et[c][L]*tok the mean is, from the window's
+ * per-class request counts n_c and token sums k_c (exact integers):
+ *   e_L = (sum_c (n_c*ef[c][L] + k_c*et[c][L])) / (sum_c n_c),
+ * summed in class order (p_L likewise with pf, pt).  The LP of the interval
+ * (solve_cell with these e, p and the region's q) gives x and thresholds;
+ * then the interval's requests are replayed as in orc_simulate and pushed,
+ * in request order, into their level's window.  Outputs per cell
+ * (r*T + t)*X + j: the solution and the cell totals.  Requests: global
+ * seg_offsets [R*T+1]; request g's tokens at tokens[L][g], flags[g].        */
+int orc_closed_loop(int n, int R, int64_t T, int X,
+                    const double *k0, const double *kmin, const double *kmax, const double *xi,
+                    const double *e_prior, const double *p_prior, const double *q, double k1, double pue,
+                    uint64_t seed, int n_classes, const double *ef, const double *et,
+                    const double *pf, const double *pt, int W,
+                    const int64_t *seg_offsets, const uint16_t *tokens, int64_t pitch, const uint8_t *flags,
+                    double *x_out, uint64_t *thr_out, uint8_t *status_out, double *prof_out,
+                    uint64_t *cnt, uint64_t *tok, double *energy, double *time_s, double *carbon, double *quality)
+{
+    if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1 || W < 1) return 1;
+    if (n_classes < 1 || n_classes > ORC_MAX_CLASSES) return 1;
+    const int NC = n_classes;
+    int *ring_c = (int *)malloc(sizeof(int) * (size_t)n * W);
+    uint32_t *ring_t = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)n * W);
+    for (int r = 0; r < R; ++r) {
+        for (int j = 0; j < X; ++j) {
+            int head[ORC_MAX_LEVELS], size[ORC_MAX_LEVELS];
+            uint64_t wn[ORC_MAX_LEVELS][ORC_MAX_CLASSES], wk[ORC_MAX_LEVELS][ORC_MAX_CLASSES];
+            memset(wn, 0, sizeof(wn)); memset(wk, 0, sizeof(wk));
+            for (int L = 0; L < n; ++L) { head[L] = 0; size[L] = 0; }
+            for (int64_t t = 0; t < T; ++t) {
+                const int64_t s = (int64_t)r * T + t;
+                const int64_t cell = s * X + j;
+                double e[ORC_MAX_LEVELS], p[ORC_MAX_LEVELS];
+                for (int L = 0; L < n; ++L) {
+                    uint64_t m = 0;
+                    for (int c = 0; c < NC; ++c) m += wn[L][c];
+                    if (m == 0) {
+                        e[L] = e_prior[(size_t)r * n + L];
+                        p[L] = p_prior[(size_t)r * n + L];
+                    } else {
+                        double se = 0.0, sp = 0.0;
+                        for (int c = 0; c < NC; ++c) {
+                            se = se + ((double)wn[L][c] * ef[c * 8 + L] + (double)wk[L][c] * et[c * 8 + L]);
+                            sp = sp + ((double)wn[L][c] * pf[c * 8 + L] + (double)wk[L][c] * pt[c * 8 + L]);
+                        }
+                        e[L] = se / (double)m;
+                        p[L] = sp / (double)m;
+                    }
+                }
+                for (int L = 0; L < n; ++L) {          /* profiles used: [cell][2][n] */
+                    prof_out[(cell * 2 + 0) * n + L] = e[L];
+                    prof_out[(cell * 2 + 1) * n + L] = p[L];
+                }
+                /* the interval's LP with the closed-loop profile */
+                orc_problem P = { n, R, 1, 0, NC, 1, &k0[s], &kmin[r], &kmax[r], &xi[j], e, p,
+                                  &q[(size_t)r * n], k1, pue, ORC_SCHEME_SPROUT, 0 };
+                double xs[ORC_MAX_LEVELS], obj, qlb; int vid, ml; uint64_t Tl[ORC_MAX_LEVELS];
+                int st = solve_cell(&P, 0, 0, xs, &obj, &qlb, &vid, Tl, &ml);
+                for (int i = 0; i < n; ++i) x_out[cell * n + i] = xs[i];
+                for (int i = 0; i + 1 < n; ++i) thr_out[cell * (n - 1) + i] = Tl[i];
+                status_out[cell] = (uint8_t)st;
+                uint64_t *cn = cnt + (size_t)cell * NC * n, *tk = tok + (size_t)cell * NC * n;
+                memset(cn, 0, sizeof(uint64_t) * NC * n);
+                memset(tk, 0, sizeof(uint64_t) * NC * n);
+                double E = 0.0, Tm = 0.0, Cb = 0.0, Q = 0.0;
+                const double kp = k0[s] * pue;
+                if (st == 0) {
+                    for (int64_t g = seg_offsets[s]; g < seg_offsets[s + 1]; ++g) {
+                        const uint32_t w = orc_draw_word(seed, (uint64_t)g);
+                        int pinned = 0, cls = 0;
+                        if (flags) { pinned = flags[g] & 1; cls = (flags[g] >> 1) & 3; }
+                        if (cls >= NC) continue;
+                        const int L = orc_select_level(n, xs, w, pinned);
+                        const uint32_t tl = tokens[(size_t)L * pitch + g];
+                        const double el = ef[cls * 8 + L] + et[cls * 8 + L] * (double)tl;
+                        const double pl = pf[cls * 8 + L] + pt[cls * 8 + L] * (double)tl;
+                        E += el; Tm += pl; Cb += orc_request_carbon(kp, k1, el, pl); Q += q[(size_t)r * n + L];
+                        cn[cls * n + L] += 1; tk[cls * n + L] += tl;
+                        /* push into level L's window (FIFO of the last W) */
+                        int slot = head[L];
+                        if (size[L] == W) {
+                            wn[L][ring_c[L * W + slot]] -= 1;
+                            wk[L][ring_c[L * W + slot]] -= ring_t[L * W + slot];
+                        } else {
+                            size[L] += 1;
+                        }
+                        ring_c[L * W + slot] = cls;
+                        ring_t[L * W + slot] = tl;
+                        wn[L][cls] += 1;
+                        wk[L][cls] += tl;
+                        head[L] = (slot + 1) % W;
+                    }
+                }
+                energy[cell] = E; time_s[cell] = Tm; carbon[cell] = Cb; quality[cell] = Q;
+            }
+        }
+    }
+    free(ring_c); free(ring_t);
+    return 0;
+}

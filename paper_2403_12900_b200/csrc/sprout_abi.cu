@@ -200,6 +200,53 @@ sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *P, double *
     return st;
 }
 
+sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int32_t window,
+                                          const sprout_trace *trace, const sprout_cost_model *cost,
+                                          const sprout_lp_solution *solution, const sprout_cell_totals *totals,
+                                          double *profile_out, sprout_stream stream) {
+    sprout_status st = validate_problem(problem);
+    if (st == SPROUT_OK) st = validate_solution(problem, solution);
+    if (st == SPROUT_OK) st = validate_trace(problem, trace);
+    if (st == SPROUT_OK) st = validate_cost(cost);
+    if (st != SPROUT_OK) return st;
+    if (!totals || !totals->trace_status) return SPROUT_ERR_INVALID_ARGUMENT;
+    const int64_t S = (int64_t)problem->n_regions * problem->n_intervals;
+    if (problem->first_segment != 0 || problem->n_segments != S || problem->profile_per_interval != 0)
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    if (window < 1 || window > 4096 || (int64_t)problem->n_levels * window * 4 > 192 * 1024)
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    if (S > 0 && (!totals->cnt || !totals->tok || !totals->energy_kwh || !totals->time_s || !totals->carbon_g ||
+                  !totals->quality))
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    if (profile_out && !aligned(profile_out, 8)) return SPROUT_ERR_INVALID_ARGUMENT;
+    ClosedArgs a{};
+    a.n = problem->n_levels; a.R = problem->n_regions; a.X = problem->n_xi; a.NC = cost->n_classes; a.W = window;
+    a.T = problem->n_intervals;
+    a.k0 = problem->k0; a.kmin = problem->k0_min; a.kmax = problem->k0_max; a.xi = problem->xi;
+    a.e = problem->e; a.p = problem->p; a.q = problem->q; a.k1 = problem->k1; a.pue = problem->pue;
+    {
+        uint32_t k0 = (uint32_t)cost->seed, k1 = (uint32_t)(cost->seed >> 32);
+        for (int r = 0; r < 10; ++r) { a.rk0[r] = k0; a.rk1[r] = k1; k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    }
+    std::memcpy(a.cost.ef, cost->ef, sizeof(cost->ef));
+    std::memcpy(a.cost.et, cost->et, sizeof(cost->et));
+    std::memcpy(a.cost.pf, cost->pf, sizeof(cost->pf));
+    std::memcpy(a.cost.pt, cost->pt, sizeof(cost->pt));
+    a.first_request = trace->first_request; a.seg_offsets = trace->seg_offsets; a.tokens = trace->tokens;
+    a.pitch = trace->plane_pitch; a.flags = trace->flags;
+    a.x = solution->x; a.objective = solution->objective; a.q_lb = solution->q_lb; a.profile = profile_out;
+    a.vertex = solution->vertex; a.cell_status = solution->cell_status; a.max_level = solution->max_level;
+    a.threshold = solution->threshold;
+    a.cnt = totals->cnt; a.tok = totals->tok; a.energy = totals->energy_kwh; a.time_s = totals->time_s;
+    a.carbon = totals->carbon_g; a.quality = totals->quality; a.trace_status = totals->trace_status;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(totals->trace_status, 0, 4, s) != cudaSuccess) return SPROUT_ERR_CUDA;
+    int launches = 0;
+    st = cuda_status(launch_closed_loop(a, s, &launches));
+    if (st == SPROUT_OK) g_last_launches = launches;
+    return st;
+}
+
 size_t sprout_workspace_bytes(const sprout_lp_problem *problem, const sprout_trace *trace) {
     if (validate_problem(problem) != SPROUT_OK) return 0;
     (void)trace;

@@ -53,6 +53,26 @@ struct LpArgs {
     int grid_den;              // D of the static grid (scheme 2)
 };
 
+struct ClosedArgs {             // closed-loop profiles (closed_loop.cu)
+    int n, R, X, NC, W;
+    int64_t T;
+    const double *k0, *kmin, *kmax, *xi, *e, *p, *q;   // e, p: priors [R][n]
+    double k1, pue;
+    uint32_t rk0[10], rk1[10];
+    CostConst cost;
+    uint64_t first_request;
+    const int64_t *seg_offsets;
+    const uint16_t *tokens;
+    int64_t pitch;
+    const uint8_t *flags;
+    double *x, *objective, *q_lb, *profile;            // profile may be NULL: [cells][2][n]
+    uint8_t *vertex, *cell_status, *max_level;
+    uint32_t *threshold;
+    uint64_t *cnt, *tok;
+    double *energy, *time_s, *carbon, *quality;
+    uint32_t *trace_status;
+};
+
 struct EvalArgs {               // evaluator trigger sweep (evaluator.cu)
     int R, B, H, F;
     int grace_samples;         // least s >= 0 with s * dt >= grace (fp64, as the definition reads)
@@ -164,6 +184,7 @@ size_t reduce_workspace_bytes(int n, int X, int R, int64_t T, int64_t first_segm
 cudaError_t launch_reduce(ReduceArgs &a, void *ws, cudaStream_t stream, int *launches);
 cudaError_t launch_generate(const GenArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_evaluator(const EvalArgs &a, cudaStream_t stream, int *launches);
+cudaError_t launch_closed_loop(const ClosedArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_select_static(const SelectArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_check_cells(const uint8_t *status, int64_t n_cells, uint32_t *out, cudaStream_t stream, int *launches);
 

@@ -99,6 +99,15 @@ class Sweep:
         else:
             S.simulate_trace(self.dp, self.sol, self.trace, self.cost, self.totals, self.ws, lv, stream)
 
+    def closed_loop(self, window: int, profile: bool = False, stream=None):
+        """Closed-loop profiles (NEXT-1): steps 1-2 as a causal scan per
+        (region, xi) chain; the segment statistics come from simulate()."""
+        prof = None
+        if profile:
+            prof = torch.zeros((self.dp.cells, 2, self.prob_host.n), dtype=torch.float64, device=self.device)
+        S.simulate_closed_loop(self.dp, window, self.trace, self.cost, self.sol, self.totals, prof, stream)
+        return prof
+
     def reduce(self, stream=None):
         S.reduce_totals(self.dp, self.sol, self.totals, self.n_classes, self.group, self.rws, stream)
 

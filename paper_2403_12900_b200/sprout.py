@@ -108,20 +108,23 @@ class EvaluatorProblem(C.Structure):
 
 
 _lib.sprout_evaluator_sweep.argtypes = [_P(EvaluatorProblem), _vp, _vp]
+_lib.sprout_simulate_closed_loop.argtypes = [_P(LpProblem), C.c_int32, _P(Trace), _P(CostModel), _P(LpSolution),
+                                             _P(CellTotals), _vp, _vp]
 _lib.sprout_solve_scheme.argtypes = [_P(LpProblem), C.c_int32, C.c_int32, _P(LpSolution), _vp]
 _lib.sprout_static_grid_size.argtypes = [C.c_int32, C.c_int32]
 _lib.sprout_static_grid_size.restype = C.c_int64
 _lib.sprout_select_static.argtypes = [_P(LpProblem), C.c_int32, C.c_double, _vp, _vp, _vp, _vp]
 for _fn in ("sprout_solve_directives", "sprout_simulate_trace", "sprout_reduce_totals", "sprout_check_cells",
             "sprout_sweep_host", "sprout_generate_trace", "sprout_solve_scheme", "sprout_select_static",
-            "sprout_simulate_trace_bounded", "sprout_evaluator_sweep"):
+            "sprout_simulate_trace_bounded", "sprout_evaluator_sweep", "sprout_simulate_closed_loop"):
     getattr(_lib, _fn).restype = C.c_int
 
 EXPORTS = ["sprout_solve_directives", "sprout_workspace_bytes", "sprout_simulate_trace", "sprout_group_stat_count",
            "sprout_reduce_workspace_bytes", "sprout_reduce_totals", "sprout_check_cells",
            "sprout_sweep_workspace_bytes", "sprout_sweep_host", "sprout_generate_trace",
            "sprout_last_launch_count", "sprout_status_string", "sprout_solve_scheme", "sprout_static_grid_size",
-           "sprout_select_static", "sprout_simulate_trace_bounded", "sprout_evaluator_sweep"]
+           "sprout_select_static", "sprout_simulate_trace_bounded", "sprout_evaluator_sweep",
+           "sprout_simulate_closed_loop"]
 
 # competing schemes, include/sprout.h SPROUT_SCHEME_*
 SCHEME_SPROUT, SCHEME_CO2_OPT, SCHEME_STATIC_GRID = 0, 1, 2
@@ -351,6 +354,14 @@ def evaluator_sweep(k2: torch.Tensor, k2_max: torch.Tensor, n_intervals: int, in
                          _ptr(k2_max), b.ctypes.data, len(t), int(fallback), t.ctypes.data, float(grace_hours),
                          float(eval_kwh), float(pue))
     _check("sprout_evaluator_sweep", _lib.sprout_evaluator_sweep(C.byref(P), _ptr(out), _stream(stream)))
+
+
+def simulate_closed_loop(prob: DeviceProblem, window: int, trace: DeviceTrace, cost: CostModel, sol: Solution,
+                         totals: Totals, profile_out: Optional[torch.Tensor] = None, stream=None) -> None:
+    p, t, s, tt = prob.c(), trace.c(), sol.c(), totals.c()
+    _check("sprout_simulate_closed_loop",
+           _lib.sprout_simulate_closed_loop(C.byref(p), int(window), C.byref(t), C.byref(cost), C.byref(s),
+                                            C.byref(tt), _ptr(profile_out), _stream(stream)))
 
 
 def check_cells(prob: DeviceProblem, sol: Solution, stream=None) -> int:
