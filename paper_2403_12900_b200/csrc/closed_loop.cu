@@ -25,23 +25,26 @@ namespace sprout {
 
 constexpr int kClThreads = 256;
 constexpr int kClWarps = kClThreads / 32;
+constexpr int kClPiece = 8192;   // requests per piece (a multiple of 4 * 32 * kClWarps)
 
-template <int N>
+template <int N, int NCM>   // NCM: class bound (1, or kMaxClasses)
 __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_constant__ ClosedArgs a) {
-    extern __shared__ uint32_t ring[];                      // [N][W] (class << 16 | tokens)
-    __shared__ unsigned long long wsum[N][kMaxClasses][2];  // window: requests, tokens per (level, class)
-    __shared__ unsigned long long csum[kMaxClasses][N][2];  // the interval's cell: requests, tokens
+    extern __shared__ uint32_t ring[];                      // [N][W] (class << 16 | tokens), then buf
+    uint32_t *buf = ring + N * a.W;                         // [kClPiece] (level << 24 | class << 16 | tokens)
+    __shared__ unsigned long long wsum[N][NCM][2];  // window: requests, tokens per (level, class)
+    __shared__ unsigned long long csum[NCM][N][2];  // the interval's cell: requests, tokens
     __shared__ int head[N], size[N];
     __shared__ uint32_t thr_s[N > 1 ? N - 1 : 1];
     __shared__ int ml_s, ok_s;
     __shared__ int wcount[kClWarps][N];
+    __shared__ uint32_t slots[kClWarps][NCM * N * 4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int chain = blockIdx.x;
     const int r = chain / a.X, j = chain % a.X;
     const int W = a.W, NC = a.NC;
     const CostConst &cost = a.cost;
     if (tid < N) { head[tid] = 0; size[tid] = 0; }
-    for (int i = tid; i < N * kMaxClasses * 2; i += kClThreads) (&wsum[0][0][0])[i] = 0ull;
+    for (int i = tid; i < N * NCM * 2; i += kClThreads) (&wsum[0][0][0])[i] = 0ull;
     __syncthreads();
     uint32_t err = 0u;
     for (int64_t t = 0; t < a.T; ++t) {
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
             ml_s = o.max_level;
             ok_s = o.status == SPROUT_CELL_OK;
         }
-        for (int i = tid; i < kMaxClasses * N * 2; i += kClThreads) (&csum[0][0][0])[i] = 0ull;
+        for (int i = tid; i < NCM * N * 2; i += kClThreads) (&csum[0][0][0])[i] = 0ull;
         __syncthreads();
         const bool cell_ok = ok_s;
         uint32_t T[N > 1 ? N - 1 : 1];
@@ -94,124 +97,193 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
         for (int i = 0; i + 1 < N; ++i) T[i] = thr_s[i];
         const int ml = ml_s;
         const int64_t s0 = a.seg_offsets[s], s1 = a.seg_offsets[s + 1];
-        uint32_t cc[kMaxClasses][N], ct[kMaxClasses][N];
+        uint32_t cc[NCM][N], ct[NCM][N];
 #pragma unroll
-        for (int c = 0; c < kMaxClasses; ++c)
+        for (int c = 0; c < NCM; ++c)
 #pragma unroll
             for (int L = 0; L < N; ++L) { cc[c][L] = 0u; ct[c][L] = 0u; }
         if (cell_ok) {
-            int64_t nchunk = 0;
-            for (int64_t base = s0; base < s1; base += kClThreads, ++nchunk) {
-                const int64_t rq = base + tid;
-                const bool inr = rq < s1;
-                int lev = -1;
-                uint32_t cls = 0u, tl = 0u;
-                if (inr) {
-                    const uint64_t g = a.first_request + (uint64_t)rq;
-                    const uint64_t blk = g >> 2;
-                    const Philox4 d = philox4x32_10_rk((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, a.rk0, a.rk1);
-                    const uint32_t k3 = (uint32_t)(g & 3u);
-                    const uint32_t w = k3 == 0 ? d.v[0] : k3 == 1 ? d.v[1] : k3 == 2 ? d.v[2] : d.v[3];
-                    uint32_t pin = 0u;
-                    if (a.flags) {
-                        const uint32_t fb = a.flags[rq];
-                        pin = fb & 1u;
-                        cls = (fb >> 1) & 3u;
-                    }
-                    if (cls >= (uint32_t)NC) {
-                        err |= SPROUT_TRACE_BAD_CLASS;
-                    } else {
-                        int L = 0;
-#pragma unroll
-                        for (int i = 0; i + 1 < N; ++i) L += (w >= T[i]) ? 1 : 0;
-                        L = pin ? 0 : min(L, ml);
-                        lev = L;
-                        tl = a.tokens[(size_t)L * a.pitch + rq];
-#pragma unroll
-                        for (int c = 0; c < kMaxClasses; ++c)
-#pragma unroll
-                            for (int LL = 0; LL < N; ++LL) {
-                                const bool hit = (uint32_t)c == cls && LL == L;
-                                cc[c][LL] += hit ? 1u : 0u;
-                                ct[c][LL] += hit ? tl : 0u;
-                            }
-                    }
-                }
-                // window push in request order: rank among the chunk's level-L requests
-                uint32_t bal[N];
+            // Pieces of up to kClPiece requests, aligned on global quads (4 requests per Philox
+            // call).  Pass A: warp w takes a contiguous run of the piece's quads, 128 requests per
+            // step (lane l draws quad l of the step and hands the words out by shuffles), selects
+            // every request's level, accumulates the cell and stores (level, class, tokens) in
+            // shared memory, counting its level-L requests.  One barrier; then every warp knows
+            // how many level-L requests precede its run (request order), and pass B re-walks the
+            // run to write the last W of each level into the ring.
+            const uint64_t gs0 = a.first_request + (uint64_t)s0, gs1 = a.first_request + (uint64_t)s1;
+            const uint64_t q0 = gs0 >> 2, q1 = (gs1 + 3) >> 2;
+            for (uint64_t pq = q0; pq < q1; pq += kClPiece / 4) {
+                const uint64_t pq1 = min(q1, pq + kClPiece / 4);
+                const uint64_t nq = pq1 - pq;
+                const uint64_t per_w = ((nq + kClWarps * 32 - 1) / (kClWarps * 32)) * 32;   // quads per warp
+                const uint64_t wq0 = min(pq1, pq + per_w * warp), wq1 = min(pq1, wq0 + per_w);
+                int cntL[N];
+                int dn[N][NCM], dk[N][NCM];   // this lane's window deltas in the piece
 #pragma unroll
                 for (int L = 0; L < N; ++L) {
-                    bal[L] = __ballot_sync(0xFFFFFFFFu, lev == L);
-                    if (lane == 0) wcount[warp][L] = __popc(bal[L]);
+                    cntL[L] = 0;
+#pragma unroll
+                    for (int c = 0; c < NCM; ++c) { dn[L][c] = 0; dk[L][c] = 0; }
+                }
+                for (uint64_t qb = wq0; qb < wq1; qb += 32) {
+                    // the block's tokens at every level and its flags are loaded first (independent,
+                    // coalesced loads in flight together; the level only selects among them)
+                    uint32_t tk4[4][N], fb4[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t g = qb * 4 + 32 * k + lane;
+                        const bool ld = g >= gs0 && g < gs1;
+                        const int64_t rq = (int64_t)(g - a.first_request);
+#pragma unroll
+                        for (int L = 0; L < N; ++L) tk4[k][L] = ld ? (uint32_t)__ldcs(a.tokens + (size_t)L * a.pitch + rq) : 0u;
+                        fb4[k] = (ld && a.flags) ? (uint32_t)__ldcs(a.flags + rq) : 0u;
+                    }
+                    const uint64_t myq = qb + lane;
+                    Philox4 d = philox4x32_10_rk((uint32_t)myq, (uint32_t)(myq >> 32), 0u, 0u, a.rk0, a.rk1);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int src = 8 * k + (lane >> 2);
+                        const uint32_t v0 = __shfl_sync(0xFFFFFFFFu, d.v[0], src);
+                        const uint32_t v1 = __shfl_sync(0xFFFFFFFFu, d.v[1], src);
+                        const uint32_t v2 = __shfl_sync(0xFFFFFFFFu, d.v[2], src);
+                        const uint32_t v3 = __shfl_sync(0xFFFFFFFFu, d.v[3], src);
+                        const uint32_t sel = lane & 3u;
+                        const uint32_t w = sel == 0 ? v0 : sel == 1 ? v1 : sel == 2 ? v2 : v3;
+                        const uint64_t g = qb * 4 + 32 * k + lane;
+                        const bool qin = qb + (uint64_t)(8 * k + (lane >> 2)) < wq1;   // quad of this warp
+                        const bool inr = qin && g >= gs0 && g < gs1;
+                        const int64_t rq = (int64_t)(g - a.first_request);
+                        int lev = -1;
+                        uint32_t cls = 0u, tl = 0u;
+                        if (inr) {
+                            const uint32_t pin = fb4[k] & 1u;
+                            cls = (fb4[k] >> 1) & 3u;
+                            if (cls >= (uint32_t)NC) {
+                                err |= SPROUT_TRACE_BAD_CLASS;
+                            } else {
+                                int L = 0;
+#pragma unroll
+                                for (int i = 0; i + 1 < N; ++i) L += (w >= T[i]) ? 1 : 0;
+                                L = pin ? 0 : min(L, ml);
+                                lev = L;
+                                tl = tk4[k][0];
+#pragma unroll
+                                for (int LL = 1; LL < N; ++LL) tl = L == LL ? tk4[k][LL] : tl;
+#pragma unroll
+                                for (int c = 0; c < NCM; ++c)
+#pragma unroll
+                                    for (int LL = 0; LL < N; ++LL) {
+                                        const bool hit = (uint32_t)c == cls && LL == L;
+                                        cc[c][LL] += hit ? 1u : 0u;
+                                        ct[c][LL] += hit ? tl : 0u;
+                                    }
+                            }
+                        }
+                        const uint64_t pos = (qb - pq) * 4 + 32 * k + lane;   // piece-relative slot
+                        if (qin) buf[pos] = lev < 0 ? 0xFF000000u : ((uint32_t)lev << 24) | (cls << 16) | tl;
+#pragma unroll
+                        for (int L = 0; L < N; ++L) cntL[L] += __popc(__ballot_sync(0xFFFFFFFFu, lev == L));
+                    }
+                }
+                if (lane < N) {
+                    int v = cntL[0];
+#pragma unroll
+                    for (int L = 1; L < N; ++L) v = lane == L ? cntL[L] : v;
+                    wcount[warp][lane] = v;
                 }
                 __syncthreads();
-                if (lev >= 0) {
-                    int before = 0, total = 0;
-                    for (int w2 = 0; w2 < kClWarps; ++w2) {
-                        const int c2 = wcount[w2][lev];
-                        before += w2 < warp ? c2 : 0;
-                        total += c2;
-                    }
-                    uint32_t bl = bal[0];
+                int before[N], total[N];
 #pragma unroll
-                    for (int L = 1; L < N; ++L) bl = lev == L ? bal[L] : bl;
-                    const int rank = before + __popc(bl & ((1u << lane) - 1u));
-                    if (rank >= total - W) ring[lev * W + (head[lev] + rank) % W] = (cls << 16) | tl;
+                for (int L = 0; L < N; ++L) {
+                    before[L] = 0;
+                    total[L] = 0;
+                    for (int w2 = 0; w2 < kClWarps; ++w2) {
+                        before[L] += w2 < warp ? wcount[w2][L] : 0;
+                        total[L] += wcount[w2][L];
+                    }
+                }
+                // only the last W requests of each level in the piece enter the ring: a warp
+                // whose run ends before them has nothing to write
+                bool any = false;
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    int mine = 0;
+                    for (int w2 = 0; w2 < kClWarps; ++w2) mine += w2 == warp ? wcount[w2][L] : 0;
+                    any = any || (before[L] + mine > total[L] - W && mine > 0);
+                }
+                for (uint64_t qb = wq0; any && qb < wq1; qb += 32) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t pos = (qb - pq) * 4 + 32 * k + lane;
+                        const bool qin = qb + (uint64_t)(8 * k + (lane >> 2)) < wq1;
+                        const uint32_t v = qin ? buf[pos] : 0xFF000000u;
+                        const int lev = (int)(v >> 24);
+#pragma unroll
+                        for (int L = 0; L < N; ++L) {
+                            const uint32_t bl = __ballot_sync(0xFFFFFFFFu, lev == L);
+                            if (lev == L) {
+                                const int rank = before[L] + __popc(bl & ((1u << lane) - 1u));
+                                if (rank >= total[L] - W) {
+                                    // the slot's previous entry (from before this piece) leaves the
+                                    // window: occupied iff the ring was full or the slot is below its fill
+                                    const int slot = (int)(((int64_t)head[L] + rank) % W);
+                                    if (size[L] == W || slot < size[L]) {
+                                        const uint32_t old = ring[L * W + slot];
+                                        const int oc = (int)(old >> 16);
+#pragma unroll
+                                        for (int c = 0; c < NCM; ++c)
+                                            if (c == oc) { dn[L][c] -= 1; dk[L][c] -= (int)(old & 0xFFFFu); }
+                                    }
+                                    ring[L * W + slot] = v & 0x00FFFFFFu;
+#pragma unroll
+                                    for (int c = 0; c < NCM; ++c)
+                                        if ((uint32_t)c == ((v >> 16) & 0xFFu)) { dn[L][c] += 1; dk[L][c] += (int)(v & 0xFFFFu); }
+                                }
+                            }
+                            before[L] += __popc(bl);
+                        }
+                    }
+                }
+                // fold the piece: per-warp sums into slots, then one thread per value adds the
+                // 8 warps (no shared atomics; every sum is an exact integer)
+#pragma unroll
+                for (int c = 0; c < NCM; ++c) {
+                    if (c >= NC) break;
+#pragma unroll
+                    for (int L = 0; L < N; ++L) {
+                        const uint32_t sc = __reduce_add_sync(0xFFFFFFFFu, cc[c][L]);
+                        const uint32_t st = __reduce_add_sync(0xFFFFFFFFu, ct[c][L]);
+                        const int sn = (int)__reduce_add_sync(0xFFFFFFFFu, (uint32_t)dn[L][c]);
+                        const int sk = (int)__reduce_add_sync(0xFFFFFFFFu, (uint32_t)dk[L][c]);
+                        if (lane == 0) {
+                            const int v = (c * N + L) * 4;
+                            slots[warp][v + 0] = sc; slots[warp][v + 1] = st;
+                            slots[warp][v + 2] = (uint32_t)sn; slots[warp][v + 3] = (uint32_t)sk;
+                        }
+                        cc[c][L] = 0u; ct[c][L] = 0u;
+                    }
                 }
                 __syncthreads();
                 if (tid < N) {
-                    int total = 0;
-                    for (int w2 = 0; w2 < kClWarps; ++w2) total += wcount[w2][tid];
-                    head[tid] = (head[tid] + total) % W;
-                    size[tid] = min(size[tid] + total, W);
+                    int tt = total[0];
+#pragma unroll
+                    for (int L = 1; L < N; ++L) tt = tid == L ? total[L] : tt;
+                    head[tid] = (int)(((int64_t)head[tid] + tt) % W);
+                    size[tid] = min(size[tid] + tt, W);
+                }
+                for (int v = tid; v < NC * N; v += kClThreads) {
+                    const int c = v / N, L = v % N;
+                    unsigned long long sc = 0, st = 0;
+                    long long sn = 0, sk = 0;
+                    for (int w2 = 0; w2 < kClWarps; ++w2) {
+                        sc += slots[w2][v * 4 + 0]; st += slots[w2][v * 4 + 1];
+                        sn += (int)slots[w2][v * 4 + 2]; sk += (int)slots[w2][v * 4 + 3];
+                    }
+                    csum[c][L][0] += sc; csum[c][L][1] += st;
+                    wsum[L][c][0] = (unsigned long long)((long long)wsum[L][c][0] + sn);
+                    wsum[L][c][1] = (unsigned long long)((long long)wsum[L][c][1] + sk);
                 }
                 __syncthreads();
-                if ((nchunk & 4095) == 4095) {   // fold the 32-bit sums before they can overflow
-#pragma unroll
-                    for (int c = 0; c < kMaxClasses; ++c)
-#pragma unroll
-                        for (int L = 0; L < N; ++L) {
-                            const uint32_t sc = __reduce_add_sync(0xFFFFFFFFu, cc[c][L]);
-                            const uint32_t st = __reduce_add_sync(0xFFFFFFFFu, ct[c][L]);
-                            if (lane == 0 && (sc | st)) { atomicAdd(&csum[c][L][0], (unsigned long long)sc);
-                                                          atomicAdd(&csum[c][L][1], (unsigned long long)st); }
-                            cc[c][L] = 0u; ct[c][L] = 0u;
-                        }
-                }
-            }
-        }
-        // the interval's cell totals
-#pragma unroll
-        for (int c = 0; c < kMaxClasses; ++c)
-#pragma unroll
-            for (int L = 0; L < N; ++L) {
-                const uint32_t sc = __reduce_add_sync(0xFFFFFFFFu, cc[c][L]);
-                const uint32_t st = __reduce_add_sync(0xFFFFFFFFu, ct[c][L]);
-                if (lane == 0 && (sc | st)) { atomicAdd(&csum[c][L][0], (unsigned long long)sc);
-                                              atomicAdd(&csum[c][L][1], (unsigned long long)st); }
-            }
-        // the windows' sums for the next interval (exact integers, any order)
-        for (int i = tid; i < N * kMaxClasses * 2; i += kClThreads) (&wsum[0][0][0])[i] = 0ull;
-        __syncthreads();
-        for (int L = 0; L < N; ++L) {
-            uint32_t wn[kMaxClasses], wk[kMaxClasses];
-#pragma unroll
-            for (int c = 0; c < kMaxClasses; ++c) { wn[c] = 0u; wk[c] = 0u; }
-            for (int i = tid; i < size[L]; i += kClThreads) {
-                const uint32_t v = ring[L * W + i];
-#pragma unroll
-                for (int c = 0; c < kMaxClasses; ++c) {
-                    const bool hit = (v >> 16) == (uint32_t)c;
-                    wn[c] += hit ? 1u : 0u;
-                    wk[c] += hit ? (v & 0xFFFFu) : 0u;
-                }
-            }
-#pragma unroll
-            for (int c = 0; c < kMaxClasses; ++c) {
-                const uint32_t sn = __reduce_add_sync(0xFFFFFFFFu, wn[c]);
-                const uint32_t sk = __reduce_add_sync(0xFFFFFFFFu, wk[c]);
-                if (lane == 0 && (sn | sk)) { atomicAdd(&wsum[L][c][0], (unsigned long long)sn);
-                                              atomicAdd(&wsum[L][c][1], (unsigned long long)sk); }
             }
         }
         __syncthreads();
@@ -245,11 +317,11 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
 cudaError_t launch_closed_loop(const ClosedArgs &a, cudaStream_t stream, int *launches) {
     const int64_t chains = (int64_t)a.R * a.X;
     if (chains == 0) return cudaSuccess;
-    const size_t smem = (size_t)a.n * a.W * 4;
+    const size_t smem = ((size_t)a.n * a.W + kClPiece) * 4;
     cudaError_t e = cudaSuccess;
 #define CL_CASE(NN)                                                                                  \
     case NN: {                                                                                       \
-        auto kern = closed_loop_kernel<NN>;                                                          \
+        auto kern = a.NC == 1 ? closed_loop_kernel<NN, 1> : closed_loop_kernel<NN, kMaxClasses>;     \
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
         if (e != cudaSuccess) return e;                                                              \
         kern<<<(unsigned)chains, kClThreads, smem, stream>>>(a);                                     \
