@@ -18,6 +18,9 @@ done
 for SC in co2opt static; do
   timeout 900 python bench.py --config C4 --scheme $SC --steps 10 --warmup 3 --no-e2e --cpu-seconds 8 > gpurun_out/bench_C4_${SC}_$TAG.json 2> gpurun_out/bench_C4_${SC}_$TAG.err; echo "bench C4 $SC rc=$?"; cut -c1-300 gpurun_out/bench_C4_${SC}_$TAG.json
 done
+timeout 600 python bench.py --config C2 --closed-loop 1000 --steps 3 --warmup 3 --no-e2e > gpurun_out/bench_C2_closed_loop_$TAG.json 2>/dev/null; echo "closed loop C2 rc=$?"
+timeout 900 python bench.py --config C4 --closed-loop 1000 --steps 3 --warmup 3 --no-e2e > gpurun_out/bench_C4_closed_loop_$TAG.json 2>/dev/null; echo "closed loop C4 rc=$?"
+timeout 300 python bench.py --evaluator --steps 10 > gpurun_out/bench_evaluator_C4_$TAG.json 2>/dev/null; echo "evaluator rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "ncu-launch rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:trace_kernel -s 2 -c 1 -o gpurun_out/prof_$TAG python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu-full rc=$?"
 timeout 900 ncu --set full --clock-control none -k regex:'lp_solve|prep_kernel|reduce_stage' -s 6 -c 5 -o gpurun_out/prof_other_$TAG python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_other_$TAG.log 2>&1; echo "ncu-other rc=$?"
