@@ -290,7 +290,9 @@ __device__ __forceinline__ WarpSmem carve(uint8_t *base, const SimArgs &a) {
     WarpSmem w;
     const int entries = a.NC * a.nb + 1;
     w.wide = reinterpret_cast<unsigned long long *>(base);
-    size_t off = (size_t)entries * (a.n + 1) * 8;
+    // 16-byte aligned rows: bit 2 of a lane's row address is then free to carry the
+    // bucket table's multi-key flag (fix_offsets)
+    size_t off = ((size_t)entries * (a.n + 1) * 8 + 15) & ~(size_t)15;
     w.hist = reinterpret_cast<uint2 *>(base + off);
     off += (size_t)entries * a.nw * 32 * 4;          // a.nw = 2 * np words
     w.lut = reinterpret_cast<uint2 *>(base + off);
@@ -1496,7 +1498,7 @@ bool make_sim_plan(int n, int X, int NC, SimPlan *plan, int max_keys) {
         while (kp < kk + 1) kp <<= 1;
         const size_t entries = (size_t)NC * nb + 1;
         const bool lut = kc >= kLutMinKeys && kc <= kLutMaxKeys;
-        size_t bytes = entries * (n + 1) * 8 + entries * p.nw * 32 * 4 + (size_t)kp * 4 +
+        size_t bytes = ((entries * (n + 1) * 8 + 15) & ~(size_t)15) + entries * p.nw * 32 * 4 + (size_t)kp * 4 +
                        (lut ? (size_t)kLutBuckets * 8 : 0);
         *nb_out = nb;
         *kp_out = kp;
