@@ -1046,7 +1046,7 @@ __device__ __forceinline__ void process_ends(const SimArgs &a, const WarpSmem &W
 // L2 prefetch distance of the streaming loop, in warp iterations (one
 // iteration = 32 groups = 512 contiguous bytes per token plane)
 #ifndef SPROUT_PREFETCH_ITERS
-#define SPROUT_PREFETCH_ITERS 8
+#define SPROUT_PREFETCH_ITERS 3
 #endif
 constexpr int kPrefetchIters = SPROUT_PREFETCH_ITERS;
 
