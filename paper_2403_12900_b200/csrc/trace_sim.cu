@@ -38,6 +38,9 @@ constexpr int kPrepWarps = 4;
 #define SPROUT_TRACE_WARPS 8
 #endif
 constexpr int kMaxTraceWarps = SPROUT_TRACE_WARPS;
+#ifndef SPROUT_LUT_FIXED
+#define SPROUT_LUT_FIXED 0   // A/B only: bucket table over [0, 2^32) (no per-segment range, no clamp)
+#endif
 #ifndef SPROUT_DISABLE_X1
 #define SPROUT_DISABLE_X1 0
 #endif
@@ -340,7 +343,11 @@ struct LutGeom {
 
 __device__ __forceinline__ LutGeom lut_geometry(const WarpSmem &W, int K) {
     LutGeom g;
+#if SPROUT_LUT_FIXED
+    const uint32_t kmin = 0u;
+#else
     const uint32_t kmin = K > 0 ? W.keys[0] : 0u;
+#endif
     int s = 0;
     for (;;) {
         const uint32_t b = (s >= 32) ? 0u : (kmin & ~((1u << s) - 1u));
@@ -484,7 +491,11 @@ __device__ __forceinline__ void group_draws(int64_t v, const SimArgs &a, U8x &w)
 // table (bit 2 of `eor` flags a multi-key bucket)
 __device__ __forceinline__ uint32_t lut_offset(uint32_t w, LutGeom geo, uint32_t rowbytes, uint32_t lane_base,
                                                uint32_t &eor) {
+#if SPROUT_LUT_FIXED
+    const uint32_t d = w;   // fixed geometry: base 0, no clamp
+#else
     const uint32_t d = max(w, geo.base);
+#endif
     const uint2 e = lds64(geo.bias + ((d >> geo.s) << 3));
     eor |= e.y;
     uint32_t r;   // e.y + lane_base + (d > e.x ? rowbytes : 0): one compare, one select, one 3-input add

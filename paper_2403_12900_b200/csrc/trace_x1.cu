@@ -22,7 +22,10 @@ constexpr int kX1Warps = 8;                   // warps per CTA
 constexpr int64_t kX1Chunk = (int64_t)1 << 21; // requests per fold: <= 2^16 per lane, token sums <= 2^16 * 65535 < 2^32
 
 template <int N, bool FLAGS, bool NC2>
-__global__ void __launch_bounds__(32 * kX1Warps, 3) trace_x1_kernel(const __grid_constant__ SimArgs a) {
+#ifndef SPROUT_X1_MIN_BLOCKS
+#define SPROUT_X1_MIN_BLOCKS 3
+#endif
+__global__ void __launch_bounds__(32 * kX1Warps, SPROUT_X1_MIN_BLOCKS) trace_x1_kernel(const __grid_constant__ SimArgs a) {
     __shared__ CostConst cost;
     // per-warp 64-bit totals of a segment: [0, NC*N) cell counts, [NC*N, 2NC*N) cell tokens,
     // then tokens per level (all classes), class-1 tokens per level, valid requests,
