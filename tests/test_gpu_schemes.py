@@ -135,3 +135,35 @@ def test_sprout_pure_segments_register_path():
     for xi in ([0.0], [0.0, 0.0], [0.0, 1.0]):
         prob = dataclasses.replace(w.prob, X=len(xi), xi=np.asarray(xi, float))
         _check(w, prob, S.SCHEME_SPROUT, 0)
+
+
+@pytest.mark.parametrize("scheme", ["co2opt", "static"])
+def test_schemes_full_size_sampled(scheme):
+    """C4 at full size (10^9 requests generated on the GPU, the bench's launch
+    configuration) under CO2_Opt and the 231-point Sprout_Sta sweep; the
+    oracle replays every 1999th segment (+ first/last/largest)."""
+    w = synth.make_workload("C4")
+    if scheme == "co2opt":
+        prob, sc, D = dataclasses.replace(w.prob, X=1, xi=np.zeros(1)), S.SCHEME_CO2_OPT, 0
+    else:
+        prob, sc, D = _static(w, 20), S.SCHEME_STATIC_GRID, 20
+    sh = synth.shard(w.spec, 1, 0)
+    sw = Sweep(prob, w.cost, sh, DEV, spec=w.spec, scheme=sc, grid_den=D)
+    sw.step()
+    torch.cuda.synchronize()
+    got = sw.host()
+    assert got["trace_status"] & ~S.TRACE_SLOW_PATH == 0
+    ids = synth.sample_segments(w.spec, 0, sh.n_segments, every=1999)
+    parts, begins, ms, g0s = [], [], [], []
+    pos = 0
+    for s in ids:
+        a, b = int(w.spec.seg_offsets[s]), int(w.spec.seg_offsets[s + 1])
+        t, _ = synth.gen_tokens(w.spec, a, b)
+        parts.append(t); begins.append(pos); ms.append(b - a); g0s.append(a); pos += b - a
+    toks = np.concatenate(parts, axis=1)
+    sim = oracle.simulate(prob, w.cost, ids, np.array(begins), np.array(ms), np.array(g0s, np.uint64), toks, None,
+                          scheme=sc, grid_den=D)
+    compare_sim(got, sim, prob.X, 1, prob.n, loc=ids)
+    G = got["group"]
+    assert G[-1, 0, 0] == w.N
+    np.testing.assert_array_equal(G[-1, :, 11:14].sum(axis=1), G[-1, :, 0])
