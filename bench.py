@@ -277,6 +277,8 @@ def run_sprout(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.closed_loop and world > 1:
+        raise SystemExit("--closed-loop runs whole regions on one device (the chains are sequential); use --gpus 1")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
