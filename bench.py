@@ -277,8 +277,7 @@ def run_sprout(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    if args.closed_loop and world > 1:
-        raise SystemExit("--closed-loop runs whole regions on one device (the chains are sequential); use --gpus 1")
+
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -286,7 +285,8 @@ def run_sprout(args):
 
     w = scheme_workload(args)
     scheme = SCHEMES[args.scheme]
-    sh = synth.shard(w.spec, world, rank)
+    # closed-loop chains are per region: ranks take whole regions; otherwise request-balanced segments
+    sh = synth.shard_regions(w.spec, w.prob.T, world, rank) if args.closed_loop else synth.shard(w.spec, world, rank)
     sw = Sweep(w.prob, w.cost, sh, dev, spec=w.spec, scheme=scheme, grid_den=args.grid_den)
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()

@@ -361,8 +361,9 @@ sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *problem, do
  * the segment fields are not written -- they do not depend on the scheme,
  * sprout_simulate_trace gives them).  `profile_out` is NULL or (device)
  * [cells][2][n]: the e and p each interval's LP used.  One CTA per chain;
- * sequential in t by definition.  Requires the whole problem on this device
- * (first_segment 0, n_segments R*T), profile_per_interval 0, and
+ * sequential in t by definition.  Requires whole regions (first_segment and
+ * n_segments multiples of n_intervals: a rank may take a range of regions;
+ * outputs are indexed by local cell), profile_per_interval 0, and
  * 1 <= window <= 4096 with n*window*4 bytes <= 192 KiB.  Errors:
  * INVALID_ARGUMENT (as sprout_simulate_trace, plus the above); CUDA. */
 sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int32_t window,

@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
     __shared__ uint32_t slots[kClWarps][NCM * N * 4];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int chain = blockIdx.x;
-    const int r = chain / a.X, j = chain % a.X;
+    const int r = a.r0 + chain / a.X, j = chain % a.X;   // this call's regions: [r0, r0 + R_local)
     const int W = a.W, NC = a.NC;
     const CostConst &cost = a.cost;
     if (tid < N) { head[tid] = 0; size[tid] = 0; }
@@ -48,8 +48,9 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
     __syncthreads();
     uint32_t err = 0u;
     for (int64_t t = 0; t < a.T; ++t) {
-        const int64_t s = (int64_t)r * a.T + t;
-        const int64_t cell = s * a.X + j;
+        const int64_t s = (int64_t)r * a.T + t;                  // global segment (k0, profiles)
+        const int64_t sl = s - a.first_segment;                  // local segment (offsets, outputs)
+        const int64_t cell = sl * a.X + j;
         if (tid == 0) {
             double e[N], p[N], q[N];
 #pragma unroll
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
 #pragma unroll
         for (int i = 0; i + 1 < N; ++i) T[i] = thr_s[i];
         const int ml = ml_s;
-        const int64_t s0 = a.seg_offsets[s], s1 = a.seg_offsets[s + 1];
+        const int64_t s0 = a.seg_offsets[sl], s1 = a.seg_offsets[sl + 1];
         uint32_t cc[NCM][N], ct[NCM][N];
 #pragma unroll
         for (int c = 0; c < NCM; ++c)
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
 }
 
 cudaError_t launch_closed_loop(const ClosedArgs &a, cudaStream_t stream, int *launches) {
-    const int64_t chains = (int64_t)a.R * a.X;
+    const int64_t chains = (int64_t)a.R_local * a.X;
     if (chains == 0) return cudaSuccess;
     const size_t smem = ((size_t)a.n * a.W + kClPiece) * 4;
     cudaError_t e = cudaSuccess;

@@ -210,9 +210,11 @@ sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int3
     if (st == SPROUT_OK) st = validate_cost(cost);
     if (st != SPROUT_OK) return st;
     if (!totals || !totals->trace_status) return SPROUT_ERR_INVALID_ARGUMENT;
-    const int64_t S = (int64_t)problem->n_regions * problem->n_intervals;
-    if (problem->first_segment != 0 || problem->n_segments != S || problem->profile_per_interval != 0)
+    // whole regions only: a chain is one region's intervals in order
+    if (problem->first_segment % problem->n_intervals != 0 || problem->n_segments % problem->n_intervals != 0 ||
+        problem->profile_per_interval != 0)
         return SPROUT_ERR_INVALID_ARGUMENT;
+    const int64_t S = problem->n_segments;
     if (window < 1 || window > 4096 || (int64_t)problem->n_levels * window * 4 > 192 * 1024)
         return SPROUT_ERR_INVALID_ARGUMENT;
     if (S > 0 && (!totals->cnt || !totals->tok || !totals->energy_kwh || !totals->time_s || !totals->carbon_g ||
@@ -222,6 +224,9 @@ sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int3
     ClosedArgs a{};
     a.n = problem->n_levels; a.R = problem->n_regions; a.X = problem->n_xi; a.NC = cost->n_classes; a.W = window;
     a.T = problem->n_intervals;
+    a.first_segment = problem->first_segment;
+    a.r0 = (int)(problem->first_segment / problem->n_intervals);
+    a.R_local = (int)(problem->n_segments / problem->n_intervals);
     a.k0 = problem->k0; a.kmin = problem->k0_min; a.kmax = problem->k0_max; a.xi = problem->xi;
     a.e = problem->e; a.p = problem->p; a.q = problem->q; a.k1 = problem->k1; a.pue = problem->pue;
     {

@@ -55,7 +55,8 @@ struct LpArgs {
 
 struct ClosedArgs {             // closed-loop profiles (closed_loop.cu)
     int n, R, X, NC, W;
-    int64_t T;
+    int r0, R_local;           // regions [r0, r0 + R_local) of this call (whole regions)
+    int64_t T, first_segment;
     const double *k0, *kmin, *kmax, *xi, *e, *p, *q;   // e, p: priors [R][n]
     double k1, pue;
     uint32_t rk0[10], rk1[10];

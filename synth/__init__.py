@@ -419,6 +419,20 @@ def shard(spec: TraceSpec, world: int, rank: int) -> Shard:
                  first_request=base, n_requests=g_hi - base, seg_offsets=local)
 
 
+def shard_regions(spec: TraceSpec, T: int, world: int, rank: int) -> Shard:
+    """Contiguous whole regions per rank (closed-loop chains are per region):
+    regions [rank*R/world, (rank+1)*R/world)."""
+    off = spec.seg_offsets
+    R = (off.size - 1) // T
+    r_lo, r_hi = (rank * R) // world, ((rank + 1) * R) // world
+    s_lo, s_hi = r_lo * T, r_hi * T
+    g_lo, g_hi = int(off[s_lo]), int(off[s_hi])
+    base = (g_lo // 8) * 8
+    local = (off[s_lo:s_hi + 1] - base).astype(np.int64)
+    return Shard(rank=rank, world=world, first_segment=s_lo, n_segments=s_hi - s_lo,
+                 first_request=base, n_requests=g_hi - base, seg_offsets=local)
+
+
 def pitch_for(n_requests: int) -> int:
     """Token-plane pitch: a multiple of 8 u16 (16 B) covering n_requests."""
     return max(8, ((n_requests + 7) // 8) * 8)

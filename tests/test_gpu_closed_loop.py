@@ -42,3 +42,27 @@ def test_closed_loop_parity(name, kw, W):
     for k in ("energy", "time", "carbon", "quality"):
         np.testing.assert_allclose(got[k].reshape(-1), want[k], rtol=FP_RTOL, atol=0, err_msg=k)
     assert got["trace_status"] == 0
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_closed_loop_region_shards(world):
+    """Chains are per region, so ranks can take whole regions: every rank's
+    cells equal the single-device run's (oracle) cells bit for bit."""
+    w = synth.make_workload("C2", n_requests=50_000, n_intervals=48)
+    want = oracle.closed_loop(w.prob, w.cost, 200, w.spec.seg_offsets, *synth.host_trace(w.spec, synth.shard(w.spec, 1, 0)))
+    X, NC, n = w.prob.X, w.cost.n_classes, w.prob.n
+    for rank in range(world):
+        sh = synth.shard_regions(w.spec, w.prob.T, world, rank)
+        if sh.n_segments == 0:
+            continue
+        toks, fl = synth.host_trace(w.spec, sh)
+        sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=fl)
+        prof = sw.closed_loop(200, profile=True)
+        torch.cuda.synchronize()
+        got = sw.host()
+        lo, hi = sh.first_segment * X, (sh.first_segment + sh.n_segments) * X
+        np.testing.assert_array_equal(prof.cpu().numpy().view(np.uint64), want["profile"][lo:hi].view(np.uint64))
+        np.testing.assert_array_equal(got["x"].view(np.uint64), want["x"][lo:hi].view(np.uint64))
+        np.testing.assert_array_equal(got["cnt"].reshape(-1, NC, n), want["cnt"][lo:hi])
+        np.testing.assert_array_equal(got["tok"].reshape(-1, NC, n), want["tok"][lo:hi])
+        np.testing.assert_allclose(got["carbon"].reshape(-1), want["carbon"][lo:hi], rtol=FP_RTOL, atol=0)
