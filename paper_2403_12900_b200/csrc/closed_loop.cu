@@ -47,20 +47,41 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
     for (int i = tid; i < N * NCM * 2; i += kClThreads) (&wsum[0][0][0])[i] = 0ull;
     __syncthreads();
     uint32_t err = 0u;
+    // the chain is latency-bound on its serial part, so everything an interval
+    // reads from global memory besides its requests is loaded one interval
+    // ahead: k0, the segment's offsets; the region's constants once
+    double q_r[N], e_r[N], p_r[N];
+#pragma unroll
+    for (int L = 0; L < N; ++L) {
+        q_r[L] = a.q[(int64_t)r * N + L];
+        e_r[L] = a.e[(int64_t)r * N + L];
+        p_r[L] = a.p[(int64_t)r * N + L];
+    }
+    const double kmin_r = a.kmin[r], kmax_r = a.kmax[r], xi_j = a.xi[j];
+    const int64_t sl_first = (int64_t)r * a.T - a.first_segment;
+    double k0_nxt = a.k0[(int64_t)r * a.T];
+    int64_t off_nxt0 = a.seg_offsets[sl_first], off_nxt1 = a.seg_offsets[sl_first + 1];
     for (int64_t t = 0; t < a.T; ++t) {
         const int64_t s = (int64_t)r * a.T + t;                  // global segment (k0, profiles)
         const int64_t sl = s - a.first_segment;                  // local segment (offsets, outputs)
         const int64_t cell = sl * a.X + j;
+        const double k0_s = k0_nxt;
+        const int64_t s0 = off_nxt0, s1 = off_nxt1;
+        if (t + 1 < a.T) {
+            k0_nxt = a.k0[s + 1];
+            off_nxt0 = s1;
+            off_nxt1 = a.seg_offsets[sl + 2];
+        }
         if (tid == 0) {
             double e[N], p[N], q[N];
 #pragma unroll
             for (int L = 0; L < N; ++L) {
-                q[L] = a.q[(int64_t)r * N + L];
+                q[L] = q_r[L];
                 unsigned long long m = 0;
                 for (int c = 0; c < NC; ++c) m += wsum[L][c][0];
                 if (m == 0) {
-                    e[L] = a.e[(int64_t)r * N + L];
-                    p[L] = a.p[(int64_t)r * N + L];
+                    e[L] = e_r[L];
+                    p[L] = p_r[L];
                 } else {
                     double se = 0.0, sp = 0.0;
                     for (int c = 0; c < NC; ++c) {
@@ -77,7 +98,7 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
                 }
             }
             LpCell<N> o;
-            lp_cell<N>(a.k0[s], a.kmin[r], a.kmax[r], a.xi[j], e, p, q, a.k1, a.pue, 0, 0, j, o);
+            lp_cell<N>(k0_s, kmin_r, kmax_r, xi_j, e, p, q, a.k1, a.pue, 0, 0, j, o);
 #pragma unroll
             for (int i = 0; i < N; ++i) a.x[cell * N + i] = o.x[i];
             a.objective[cell] = o.objective;
@@ -97,7 +118,6 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
 #pragma unroll
         for (int i = 0; i + 1 < N; ++i) T[i] = thr_s[i];
         const int ml = ml_s;
-        const int64_t s0 = a.seg_offsets[sl], s1 = a.seg_offsets[sl + 1];
         uint32_t cc[NCM][N], ct[NCM][N];
 #pragma unroll
         for (int c = 0; c < NCM; ++c)
@@ -289,8 +309,7 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
         }
         __syncthreads();
         if (tid == 0) {   // cell_epilogue's formulas and order
-            const double kp = a.k0[s] * a.pue;
-            const double *qrow = a.q + (int64_t)r * N;
+            const double kp = k0_s * a.pue;
             double E = 0.0, Tm = 0.0, Q = 0.0;
             for (int c = 0; c < NC; ++c) {
 #pragma unroll
@@ -301,7 +320,7 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
                     const double n_ = (double)cn, t_ = (double)tk;
                     E += n_ * cost.ef[c][L] + t_ * cost.et[c][L];
                     Tm += n_ * cost.pf[c][L] + t_ * cost.pt[c][L];
-                    Q += n_ * qrow[L];
+                    Q += n_ * q_r[L];
                 }
             }
             a.energy[cell] = E;
