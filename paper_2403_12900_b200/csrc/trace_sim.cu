@@ -38,6 +38,12 @@ constexpr int kPrepWarps = 4;
 #define SPROUT_TRACE_WARPS 8
 #endif
 constexpr int kMaxTraceWarps = SPROUT_TRACE_WARPS;
+#ifndef SPROUT_LD_HINT
+#define SPROUT_LD_HINT 0     // A/B only: L2::256B sector-promotion hint on the token loads
+#endif
+#ifndef SPROUT_NO_PREFETCH
+#define SPROUT_NO_PREFETCH 0 // A/B only: no in-loop L2 prefetch
+#endif
 #ifndef SPROUT_LUT_FIXED
 #define SPROUT_LUT_FIXED 0   // A/B only: bucket table over [0, 2^32) (no per-segment range, no clamp)
 #endif
@@ -1112,7 +1118,15 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
     uint64_t blk = ((a.first_request + (uint64_t)v0 * 8u) >> 2) + 128u;
     auto load_at = [&](Group<N, FLAGS> &g, int it) {   // group of iteration (current + it)
 #pragma unroll
-        for (int q = 0; q < N; ++q) g.t[q] = __ldcs(reinterpret_cast<const uint4 *>(qp[q]) + 32 * it);
+        for (int q = 0; q < N; ++q) {
+#if SPROUT_LD_HINT
+            const uint4 *src = reinterpret_cast<const uint4 *>(qp[q]) + 32 * it;
+            asm volatile("ld.global.cs.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(g.t[q].x), "=r"(g.t[q].y), "=r"(g.t[q].z), "=r"(g.t[q].w) : "l"(src));
+#else
+            g.t[q] = __ldcs(reinterpret_cast<const uint4 *>(qp[q]) + 32 * it);
+#endif
+        }
         if (FLAGS) g.f = __ldcs(reinterpret_cast<const uint2 *>(fp) + 32 * it);
     };
 
@@ -1137,6 +1151,7 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
     }
     auto body = [&](auto bc, uint32_t i) {
         constexpr int b = decltype(bc)::value;
+#if !SPROUT_NO_PREFETCH
         {
             const uint32_t pf = (i + kPrefetchIters < n_mine) ? 1u : 0u;
 #pragma unroll
@@ -1144,6 +1159,7 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
                 asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p prefetch.global.L2 [%1];\n\t}"
                              ::"r"(pf), "l"(qp[q] + 512 * kPrefetchIters));
         }
+#endif
         if (i + 1 < n_mine) load_at(g[b ^ 1], 1);
         group_draws_blk(blk, a, wq[b ^ 1]);
         U8x row;
