@@ -38,6 +38,9 @@ constexpr int kPrepWarps = 4;
 #define SPROUT_TRACE_WARPS 8
 #endif
 constexpr int kMaxTraceWarps = SPROUT_TRACE_WARPS;
+#ifndef SPROUT_LOOKUP_ORDER
+#define SPROUT_LOOKUP_ORDER 0   // A/B only: placement of the next group's table lookups in the body
+#endif
 #ifndef SPROUT_LD_HINT
 #define SPROUT_LD_HINT 0     // A/B only: L2::256B sector-promotion hint on the token loads
 #endif
@@ -673,12 +676,32 @@ __device__ __forceinline__ uint32_t update_fast(const Group<N, FLAGS> &g, const 
                                                 uint32_t rowbytes, U8x &on, uint32_t &en) {
     uint32_t acc0 = 0u, acc = 0u;
     if (MODE == kModeLut) {
+#if SPROUT_LOOKUP_ORDER == 1
+        // A/B: the next group's lookups first, then the read-modify-write chain
+#pragma unroll
+        for (int k = 0; k < 8; ++k) on.v[k] = lut_offset(wn.v[k], geo, rowbytes, lane_base, en);
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) rmw_pair<N, FLAGS>(g, k, row.v[k], row.v[k + 1], acc0, acc);
+#elif SPROUT_LOOKUP_ORDER == 2
+        // A/B: four lookups ahead of each pair
+#pragma unroll
+        for (int k = 0; k < 4; ++k) on.v[k] = lut_offset(wn.v[k], geo, rowbytes, lane_base, en);
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+            rmw_pair<N, FLAGS>(g, k, row.v[k], row.v[k + 1], acc0, acc);
+            if (k + 4 < 8) {
+                on.v[k + 4] = lut_offset(wn.v[k + 4], geo, rowbytes, lane_base, en);
+                on.v[k + 5] = lut_offset(wn.v[k + 5], geo, rowbytes, lane_base, en);
+            }
+        }
+#else
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
             rmw_pair<N, FLAGS>(g, k, row.v[k], row.v[k + 1], acc0, acc);
             on.v[k] = lut_offset(wn.v[k], geo, rowbytes, lane_base, en);
             on.v[k + 1] = lut_offset(wn.v[k + 1], geo, rowbytes, lane_base, en);
         }
+#endif
     } else {
 #pragma unroll
         for (int k = 0; k < 8; k += 2) rmw_pair<N, FLAGS>(g, k, row.v[k], row.v[k + 1], acc0, acc);
