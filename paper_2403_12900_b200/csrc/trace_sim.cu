@@ -906,11 +906,7 @@ __device__ __forceinline__ void cell_epilogue(const SimArgs &a, const WarpSmem &
     int t = 0;
     for (int j = lane_id(); j < a.X; j += 32, ++t) {
         const int64_t cell = sl * a.X + j;
-        const uint32_t st = pre ? (t == 0 ? sc.st[0] : sc.st[1]) : a.cell_status[cell];
-        if (st != SPROUT_CELL_OK) {
-            zero_cell(a, cell, NC * N);
-            continue;
-        }
+        // status and level boundaries are loaded together (independent loads, one round trip)
         int bnd[N + 1];
         bnd[0] = 0;
         bnd[N] = K + 1;
@@ -923,6 +919,11 @@ __device__ __forceinline__ void cell_epilogue(const SimArgs &a, const WarpSmem &
 #pragma unroll
                 for (int L = 1; L < N; ++L) bnd[L] = a.seg_bnd[cell * (N - 1) + (L - 1)];
             }
+        }
+        const uint32_t st = pre ? (t == 0 ? sc.st[0] : sc.st[1]) : a.cell_status[cell];
+        if (st != SPROUT_CELL_OK) {
+            zero_cell(a, cell, NC * N);
+            continue;
         }
         double E = 0.0, T = 0.0, Q = 0.0;
         for (int c = 0; c < NC; ++c) {
@@ -1443,6 +1444,16 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
                     if (FLAGS) prefetch_l2(a.flags + (size_t)v * 8);
                 }
             }
+        }
+        if (!pre_cells) {   // the epilogue's per-cell metadata into L2 (the lines of the two byte ranges)
+            const int64_t c0 = sl * X;
+            const uintptr_t a0 = reinterpret_cast<uintptr_t>(a.cell_status + c0) & ~(uintptr_t)127;
+            const uintptr_t a1 = reinterpret_cast<uintptr_t>(a.cell_status + c0 + X);
+            const uintptr_t b0 = reinterpret_cast<uintptr_t>(a.seg_bnd + c0 * (N - 1)) & ~(uintptr_t)127;
+            const uintptr_t b1 = reinterpret_cast<uintptr_t>(a.seg_bnd + (c0 + X) * (N - 1));
+            const int64_t na = (int64_t)((a1 - a0 + 127) / 128), nbl = (int64_t)((b1 - b0 + 127) / 128);
+            for (int64_t ln = lane; ln < na + nbl; ln += 32)
+                prefetch_l2(reinterpret_cast<const void *>(ln < na ? a0 + 128 * ln : b0 + 128 * (ln - na)));
         }
         readout<N>(a, W, K);
         cell_epilogue<N>(a, W, sl, K, kp, qrow, true, cost, pre_cells, cur.sc);
