@@ -298,7 +298,8 @@ def run_sprout(args):
     launches = [0]
 
     def step(ev=None):
-        sw.solve(); launches[0] += S.last_launch_count()
+        if not args.closed_loop:   # the closed-loop scan solves every interval's LP itself
+            sw.solve(); launches[0] += S.last_launch_count()
         if ev is not None:
             ev[0].record(stream)
         if args.closed_loop:
@@ -366,19 +367,17 @@ def run_sprout(args):
 
     peak, peak_src = peaks()
     alg = algorithmic_bytes(w, sh)
-    if args.closed_loop:   # each (region, xi) chain reads its requests' selected-level token (+ flags)
+    if args.closed_loop:   # the trace once (the chains of a region share it) + every interval's LP outputs
         P = w.prob
         f = 1 if w.spec.has_flags else 0
-        alg = int(sh.seg_offsets[-1] - sh.seg_offsets[0]) * P.X * (2 + f) + \
-            sh.n_segments * P.X * (P.n * 8 + 8 + 8 + 4 * (P.n - 1) + 3 + w.cost.n_classes * P.n * 16 + 32)
+        alg = algorithmic_bytes(w, sh) + sh.n_segments * P.X * (P.n * 8 + 8 + 8)
     sim_avg_ms = statistics.mean(sim_ms)
     achieved = alg / (sim_avg_ms * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf):
-        d = json.load(open(tf))
-        if d.get("workload") == w.name and d.get("n_gpus", 1) == world:
-            traffic = d.get("dram_bytes_per_launch")
+    if os.path.exists(tf):   # ncu DRAM bytes per launch, keyed by the measured (config, scheme, mode, GPUs)
+        key = f"{w.name}/{args.scheme}/{'closed' if args.closed_loop else 'open'}/{world}"
+        traffic = json.load(open(tf)).get(key, {}).get("dram_bytes_per_launch")
     cpu = None
     if not args.no_cpu_baseline and world == 1 and not args.closed_loop:
         cpu = oracle_baseline(w, args.cpu_seconds, scheme, args.grid_den)
@@ -397,7 +396,8 @@ def run_sprout(args):
         "lp_cells_per_s": w.prob.C / (lp_ms * 1e-3),
         "request_cells_per_s": N * w.prob.X / (ms_per_step * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": ("sprout_simulate_closed_loop (one CTA per chain)" if args.closed_loop
+                     "traffic": traffic, "kernel": ("sprout_simulate_closed_loop (one CTA per group of xi chains "
+                                                    "of a region)" if args.closed_loop
                                                     else "sprout_simulate_trace (prep + trace_kernel, CUDA events)"),
                      "algorithmic_bytes_per_launch": alg, "launch_ms": sim_avg_ms, "peak_source": peak_src},
         "clocks": clk.summary(),

@@ -356,15 +356,20 @@ sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *problem, do
  * p_L likewise.  The interval's LP (as sprout_solve_directives) uses it; the
  * interval's requests are then selected and accounted exactly as in
  * sprout_simulate_trace, and pushed in request order into their level's
- * window.  Writes every field of `solution` and the per-cell fields of
- * `totals` (cnt, tok, energy_kwh, time_s, carbon_g, quality, trace_status;
- * the segment fields are not written -- they do not depend on the scheme,
- * sprout_simulate_trace gives them).  `profile_out` is NULL or (device)
- * [cells][2][n]: the e and p each interval's LP used.  One CTA per chain;
- * sequential in t by definition.  Requires whole regions (first_segment and
- * n_segments multiples of n_intervals: a rank may take a range of regions;
- * outputs are indexed by local cell), profile_per_interval 0, and
- * 1 <= window <= 4096 with n*window*4 bytes <= 192 KiB.  Errors:
+ * window.  Writes every field of `solution` and every field of `totals`
+ * (cells: cnt, tok, energy_kwh, time_s, carbon_g, quality; segments:
+ * seg_count, seg_pinned, seg_tok, seg_base -- the same values
+ * sprout_simulate_trace gives, they do not depend on the scheme; and
+ * trace_status), so sprout_reduce_totals can follow directly.  Invalid
+ * offsets (s0 > s1, or past n_requests) flag SPROUT_TRACE_BAD_OFFSETS and
+ * the interval is skipped: its cells and segment fields are zero and no
+ * request enters a window.  `profile_out` is NULL or (device)
+ * [cells][2][n]: the e and p each interval's LP used.  One CTA per group of
+ * up to 4 xi chains of a region (they share the requests' draws, tokens and
+ * flags); sequential in t by definition.  Requires whole regions
+ * (first_segment and n_segments multiples of n_intervals: a rank may take a
+ * range of regions; outputs are indexed by local cell), profile_per_interval
+ * 0, and 1 <= window <= 4096 with n*window*4 bytes <= 192 KiB.  Errors:
  * INVALID_ARGUMENT (as sprout_simulate_trace, plus the above); CUDA. */
 sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int32_t window,
                                           const sprout_trace *trace, const sprout_cost_model *cost,

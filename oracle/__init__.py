@@ -105,8 +105,8 @@ def _bind(L):
     L.orc_evaluator_sweep.restype = C.c_int
     L.orc_closed_loop.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                   C.c_double, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp, _dp, C.c_int,
-                                  _i64p, _u16p, C.c_int64, _u8p, _dp, _u64p, _u8p, _dp, _u64p, _u64p, _dp, _dp, _dp,
-                                  _dp]
+                                  _i64p, _u16p, C.c_int64, _u8p, _dp, _u64p, _u8p, _dp, _dp, _u64p, _u64p, _dp, _dp,
+                                  _dp, _dp]
     L.orc_closed_loop.restype = C.c_int
     return L
 
@@ -338,7 +338,7 @@ def closed_loop(prob, cost, window: int, seg_offsets, tokens, flags=None):
     fl = None if flags is None else np.ascontiguousarray(flags, dtype=np.uint8)
     cells = R * T * X
     out = dict(x=np.zeros((cells, n)), threshold=np.zeros((cells, max(n - 1, 1)), np.uint64),
-               cell_status=np.zeros(cells, np.uint8), profile=np.zeros((cells, 2, n)),
+               cell_status=np.zeros(cells, np.uint8), objective=np.zeros(cells), profile=np.zeros((cells, 2, n)),
                cnt=np.zeros((cells, NC, n), np.uint64),
                tok=np.zeros((cells, NC, n), np.uint64), energy=np.zeros(cells), time=np.zeros(cells),
                carbon=np.zeros(cells), quality=np.zeros(cells))
@@ -349,7 +349,7 @@ def closed_loop(prob, cost, window: int, seg_offsets, tokens, flags=None):
                                C.c_uint64(int(cost.seed)), NC, _p(ef, _dp), _p(et, _dp), _p(pf, _dp), _p(pt, _dp),
                                int(window), _p(off, _i64p), _p(tokens, _u16p), tokens.shape[1], _p(fl, _u8p),
                                _p(out["x"], _dp), _p(out["threshold"], _u64p), _p(out["cell_status"], _u8p),
-                               _p(out["profile"], _dp), _p(out["cnt"], _u64p), _p(out["tok"], _u64p), _p(out["energy"], _dp),
+                               _p(out["objective"], _dp), _p(out["profile"], _dp), _p(out["cnt"], _u64p), _p(out["tok"], _u64p), _p(out["energy"], _dp),
                                _p(out["time"], _dp), _p(out["carbon"], _dp), _p(out["quality"], _dp))
     if st != 0:
         raise ValueError("oracle closed_loop: invalid argument")

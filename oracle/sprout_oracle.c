@@ -788,7 +788,7 @@ int orc_closed_loop(int n, int R, int64_t T, int X,
                     uint64_t seed, int n_classes, const double *ef, const double *et,
                     const double *pf, const double *pt, int W,
                     const int64_t *seg_offsets, const uint16_t *tokens, int64_t pitch, const uint8_t *flags,
-                    double *x_out, uint64_t *thr_out, uint8_t *status_out, double *prof_out,
+                    double *x_out, uint64_t *thr_out, uint8_t *status_out, double *obj_out, double *prof_out,
                     uint64_t *cnt, uint64_t *tok, double *energy, double *time_s, double *carbon, double *quality)
 {
     if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1 || W < 1) return 1;
@@ -831,6 +831,7 @@ int orc_closed_loop(int n, int R, int64_t T, int X,
                                   &q[(size_t)r * n], k1, pue, ORC_SCHEME_SPROUT, 0 };
                 double xs[ORC_MAX_LEVELS], obj, qlb; int vid, ml; uint64_t Tl[ORC_MAX_LEVELS];
                 int st = solve_cell(&P, 0, 0, xs, &obj, &qlb, &vid, Tl, &ml);
+                obj_out[cell] = obj;
                 for (int i = 0; i < n; ++i) x_out[cell * n + i] = xs[i];
                 for (int i = 0; i + 1 < n; ++i) thr_out[cell * (n - 1) + i] = Tl[i];
                 status_out[cell] = (uint8_t)st;

@@ -7,15 +7,22 @@
 // (lp_cell.cuh, the same arithmetic as step 1), and the interval's requests
 // are replayed and pushed into their level's window.
 //
-// The chain is sequential in time by definition, so one CTA runs one chain;
-// inside an interval its 256 threads take one request each per chunk.  The
-// window of level L is a ring of the last W (class, tokens) pairs in shared
-// memory; a request's slot is fixed by its rank among the chunk's level-L
-// requests (warp ballots + a prefix over the 8 warps), so the ring holds the
-// FIFO order exactly.  With E = ef + et*tok (reading L11) the window mean is
-// a function of per-class counts and token sums -- exact integers, summed in
-// any order -- so the profile, and the LP decision it feeds, are
-// bit-identical to the oracle's.
+// A chain is sequential in time by definition; the chains of a region are
+// not, and they share everything but the thresholds: the requests' draws
+// (common random numbers, reading L10), tokens and flags.  So one CTA runs a
+// GROUP of G chains of one region: per interval, threads 0..G-1 solve the G
+// LPs; then the interval streams in pieces of kClPiece requests, each thread
+// taking 8 consecutive requests (one 128-bit load per token plane, two
+// Philox calls), and every request is selected in all G chains from the same
+// registers.  The window of (chain, level) is a ring of the last W
+// (class, tokens) entries in shared memory; a request's slot is its rank
+// among the piece's requests of that chain and level (a block-wide scan of
+// per-thread counts), so the ring keeps FIFO order exactly.  With
+// E = ef + et*tok (reading L11) the window mean is a function of per-class
+// counts and token sums -- exact integers -- so the profile, and the LP
+// decision it feeds, are bit-identical to the oracle's.  The first group of
+// each region also writes the segment statistics and the Base counterfactual
+// (they do not depend on the chain), so the call's totals are complete.
 #include <cuda_runtime.h>
 #include "sprout_device.cuh"
 #include "sprout_kernels.cuh"
@@ -25,308 +32,497 @@ namespace sprout {
 
 constexpr int kClThreads = 256;
 constexpr int kClWarps = kClThreads / 32;
-constexpr int kClPiece = 8192;   // requests per piece (a multiple of 4 * 32 * kClWarps)
+constexpr int kClPiece = 8 * kClThreads;   // requests per piece: 8 per thread
 
-template <int N, int NCM>   // NCM: class bound (1, or kMaxClasses)
+__device__ __forceinline__ uint32_t cl_half(uint4 u, int k) {   // u16 token k of a 16-byte group
+    const uint32_t w = (k >> 1) == 0 ? u.x : (k >> 1) == 1 ? u.y : (k >> 1) == 2 ? u.z : u.w;
+    return (k & 1) ? (w >> 16) : (w & 0xFFFFu);
+}
+
+// level of a draw in a chain: pinned ? 0 : min(#{i : w >= T_i}, max_level) (a6)
+template <int N>
+__device__ __forceinline__ int cl_level(uint32_t w, const uint32_t (&T)[N > 1 ? N - 1 : 1], int ml, bool pinned) {
+    int L = 0;
+#pragma unroll
+    for (int i = 0; i + 1 < N; ++i) L += (w >= T[i]) ? 1 : 0;
+    L = L < ml ? L : ml;
+    return pinned ? 0 : L;
+}
+
+constexpr int kClMaxPieces = 128;   // per-piece level counts kept for the window pass (intervals <= 2^20)
+
+// 8 consecutive requests [c0, c0 + 8) of a piece: tokens (one 128-bit load
+// per plane), flags, the 8 selection draws (two Philox calls, reading L10)
+template <int N>
+struct Chunk {
+    uint4 tk[N];
+    uint2 fw;
+    uint32_t w[8];
+};
+template <int N>
+__device__ __forceinline__ void load_chunk(const ClosedArgs &a, int64_t c0, bool any, Chunk<N> &ch) {
+    if (any) {
+#pragma unroll
+        for (int L = 0; L < N; ++L) ch.tk[L] = __ldcs(reinterpret_cast<const uint4 *>(a.tokens + (size_t)L * a.pitch + c0));
+        ch.fw = a.flags ? __ldcs(reinterpret_cast<const uint2 *>(a.flags + c0)) : make_uint2(0u, 0u);
+        const uint64_t blk = (a.first_request + (uint64_t)c0) >> 2;
+        const Philox4 d0 = philox4x32_10_rk((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, a.rk0, a.rk1);
+        const Philox4 d1 = philox4x32_10_rk((uint32_t)(blk + 1), (uint32_t)((blk + 1) >> 32), 0u, 0u, a.rk0, a.rk1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { ch.w[k] = d0.v[k]; ch.w[4 + k] = d1.v[k]; }
+    } else {
+#pragma unroll
+        for (int L = 0; L < N; ++L) ch.tk[L] = make_uint4(0u, 0u, 0u, 0u);
+        ch.fw = make_uint2(0u, 0u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ch.w[k] = 0u;
+    }
+}
+__device__ __forceinline__ uint32_t flag_byte(uint2 fw, int k) { return ((k < 4 ? fw.x : fw.y) >> (8 * (k & 3))) & 0xFFu; }
+
+// L2 prefetch of the piece starting at local request p0 (up to s1): one 128-byte
+// line per thread, 32 lines per token plane and 16 of flags
+template <int N>
+__device__ __forceinline__ void prefetch_piece(const ClosedArgs &a, int64_t p0, int64_t s1, int tid) {
+    constexpr int kLines = kClPiece * 2 / 128;   // 32 lines of one token plane
+    if (p0 >= s1) return;
+    if (tid < kLines * N) {
+        const int q = tid / kLines, l = tid % kLines;
+        const int64_t r = p0 + 64 * (int64_t)l;
+        if (r < s1) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.tokens + (size_t)q * a.pitch + r));
+    } else if (a.flags && tid < kLines * N + kLines / 2) {
+        const int64_t r = p0 + 128 * (int64_t)(tid - kLines * N);
+        if (r < s1) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.flags + r));
+    }
+}
+
+template <int N, int NCM, int G>
 __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_constant__ ClosedArgs a) {
-    extern __shared__ uint32_t ring[];                      // [N][W] (class << 16 | tokens), then buf
-    uint32_t *buf = ring + N * a.W;                         // [kClPiece] (level << 24 | class << 16 | tokens)
-    __shared__ unsigned long long wsum[N][NCM][2];  // window: requests, tokens per (level, class)
-    __shared__ unsigned long long csum[NCM][N][2];  // the interval's cell: requests, tokens
-    __shared__ int head[N], size[N];
-    __shared__ uint32_t thr_s[N > 1 ? N - 1 : 1];
-    __shared__ int ml_s, ok_s;
-    __shared__ int wcount[kClWarps][N];
-    __shared__ uint32_t slots[kClWarps][NCM * N * 4];
+    extern __shared__ uint32_t ring[];                      // [G][N][W] class << 16 | tokens
+    __shared__ unsigned long long wsum[G][N][NCM][2];       // window: requests, tokens per (chain, level, class)
+    __shared__ int head[G][N], size[G][N];
+    __shared__ uint32_t thr_s[G][N > 1 ? N - 1 : 1];
+    __shared__ int ml_s[G], ok_s[G];
+    __shared__ int seg_ok_s;
+    __shared__ uint32_t pcnt[kClMaxPieces][G * N];          // level-L requests of (chain, piece)
+    __shared__ uint32_t ctot[G * N], cfirst[G * N];         // interval totals; first piece holding a window entry
+    __shared__ uint32_t wtot[kClWarps][G * N];              // per-warp counts (window-pass scan)
+    constexpr int NCELL = G * NCM * N * 2, NDELTA = G * N * NCM * 2, NSEG = NCM * (N + 2);
+    __shared__ uint32_t part[kClWarps][NDELTA];             // per-warp window deltas of the interval
+    __shared__ unsigned long long part64[kClWarps][NCELL + NSEG];   // per-warp 64-bit cell / segment sums
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int chain = blockIdx.x;
-    const int r = a.r0 + chain / a.X, j = chain % a.X;   // this call's regions: [r0, r0 + R_local)
+    const int rl = blockIdx.x / a.n_groups, gi = blockIdx.x % a.n_groups;
+    const int r = a.r0 + rl;                                 // global region
+    const int j0 = gi * G;                                   // first xi of the group
     const int W = a.W, NC = a.NC;
+    const bool seg_writer = gi == 0;                         // one group per region writes the segment fields
     const CostConst &cost = a.cost;
-    if (tid < N) { head[tid] = 0; size[tid] = 0; }
-    for (int i = tid; i < N * NCM * 2; i += kClThreads) (&wsum[0][0][0])[i] = 0ull;
+    for (int i = tid; i < G * N; i += kClThreads) { (&head[0][0])[i] = 0; (&size[0][0])[i] = 0; }
+    for (int i = tid; i < G * N * NCM * 2; i += kClThreads) (&wsum[0][0][0][0])[i] = 0ull;
     __syncthreads();
     uint32_t err = 0u;
-    // the chain is latency-bound on its serial part, so everything an interval
-    // reads from global memory besides its requests is loaded one interval
-    // ahead: k0, the segment's offsets; the region's constants once
-    double q_r[N], e_r[N], p_r[N];
-#pragma unroll
-    for (int L = 0; L < N; ++L) {
-        q_r[L] = a.q[(int64_t)r * N + L];
-        e_r[L] = a.e[(int64_t)r * N + L];
-        p_r[L] = a.p[(int64_t)r * N + L];
-    }
-    const double kmin_r = a.kmin[r], kmax_r = a.kmax[r], xi_j = a.xi[j];
-    const int64_t sl_first = (int64_t)r * a.T - a.first_segment;
-    double k0_nxt = a.k0[(int64_t)r * a.T];
-    int64_t off_nxt0 = a.seg_offsets[sl_first], off_nxt1 = a.seg_offsets[sl_first + 1];
     for (int64_t t = 0; t < a.T; ++t) {
-        const int64_t s = (int64_t)r * a.T + t;                  // global segment (k0, profiles)
-        const int64_t sl = s - a.first_segment;                  // local segment (offsets, outputs)
-        const int64_t cell = sl * a.X + j;
-        const double k0_s = k0_nxt;
-        const int64_t s0 = off_nxt0, s1 = off_nxt1;
-        if (t + 1 < a.T) {
-            k0_nxt = a.k0[s + 1];
-            off_nxt0 = s1;
-            off_nxt1 = a.seg_offsets[sl + 2];
+        const int64_t s = (int64_t)r * a.T + t;          // global segment (k0, profiles)
+        const int64_t sl = s - a.first_segment;          // local segment (offsets, outputs)
+        const int64_t s0 = a.seg_offsets[sl], s1 = a.seg_offsets[sl + 1];
+        const double k0_s = a.k0[s];
+        const double *qrow = a.q_seg ? a.q_seg + s * N : a.q + (int64_t)r * N;
+        // ---- the G interval LPs, with the closed-loop profile ----
+        if (tid < G) {
+            const int c = tid, j = j0 + c;
+            int ok = 0;
+            if (j < a.X) {
+                const int64_t cell = sl * a.X + j;
+                double e[N], p[N], q[N];
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    q[L] = qrow[L];
+                    unsigned long long m = 0;
+                    for (int cc = 0; cc < NC; ++cc) m += wsum[c][L][cc][0];
+                    if (m == 0) {
+                        e[L] = a.e[(int64_t)r * N + L];
+                        p[L] = a.p[(int64_t)r * N + L];
+                    } else {
+                        double se = 0.0, sp = 0.0;
+                        for (int cc = 0; cc < NC; ++cc) {
+                            const double nc = (double)wsum[c][L][cc][0], kc = (double)wsum[c][L][cc][1];
+                            se = __dadd_rn(se, __dadd_rn(__dmul_rn(nc, cost.ef[cc][L]), __dmul_rn(kc, cost.et[cc][L])));
+                            sp = __dadd_rn(sp, __dadd_rn(__dmul_rn(nc, cost.pf[cc][L]), __dmul_rn(kc, cost.pt[cc][L])));
+                        }
+                        e[L] = __ddiv_rn(se, (double)m);
+                        p[L] = __ddiv_rn(sp, (double)m);
+                    }
+                    if (a.profile) {
+                        a.profile[(cell * 2 + 0) * N + L] = e[L];
+                        a.profile[(cell * 2 + 1) * N + L] = p[L];
+                    }
+                }
+                LpCell<N> o;
+                lp_cell<N>(k0_s, a.kmin[r], a.kmax[r], a.xi[j], e, p, q, a.k1, a.pue, 0, 0, j, o);
+#pragma unroll
+                for (int i = 0; i < N; ++i) a.x[cell * N + i] = o.x[i];
+                a.objective[cell] = o.objective;
+                a.q_lb[cell] = o.q_lb;
+                a.vertex[cell] = o.vertex;
+                a.cell_status[cell] = o.status;
+#pragma unroll
+                for (int i = 0; i + 1 < N; ++i) { a.threshold[cell * (N - 1) + i] = o.T[i]; thr_s[c][i] = o.T[i]; }
+                a.max_level[cell] = o.max_level;
+                ml_s[c] = o.max_level;
+                ok = o.status == SPROUT_CELL_OK;
+            }
+            ok_s[c] = ok;
         }
         if (tid == 0) {
-            double e[N], p[N], q[N];
-#pragma unroll
-            for (int L = 0; L < N; ++L) {
-                q[L] = q_r[L];
-                unsigned long long m = 0;
-                for (int c = 0; c < NC; ++c) m += wsum[L][c][0];
-                if (m == 0) {
-                    e[L] = e_r[L];
-                    p[L] = p_r[L];
-                } else {
-                    double se = 0.0, sp = 0.0;
-                    for (int c = 0; c < NC; ++c) {
-                        const double nc = (double)wsum[L][c][0], kc = (double)wsum[L][c][1];
-                        se = __dadd_rn(se, __dadd_rn(__dmul_rn(nc, cost.ef[c][L]), __dmul_rn(kc, cost.et[c][L])));
-                        sp = __dadd_rn(sp, __dadd_rn(__dmul_rn(nc, cost.pf[c][L]), __dmul_rn(kc, cost.pt[c][L])));
-                    }
-                    e[L] = __ddiv_rn(se, (double)m);
-                    p[L] = __ddiv_rn(sp, (double)m);
-                }
-                if (a.profile) {
-                    a.profile[(cell * 2 + 0) * N + L] = e[L];
-                    a.profile[(cell * 2 + 1) * N + L] = p[L];
-                }
-            }
-            LpCell<N> o;
-            lp_cell<N>(k0_s, kmin_r, kmax_r, xi_j, e, p, q, a.k1, a.pue, 0, 0, j, o);
-#pragma unroll
-            for (int i = 0; i < N; ++i) a.x[cell * N + i] = o.x[i];
-            a.objective[cell] = o.objective;
-            a.q_lb[cell] = o.q_lb;
-            a.vertex[cell] = o.vertex;
-            a.cell_status[cell] = o.status;
-#pragma unroll
-            for (int i = 0; i + 1 < N; ++i) { a.threshold[cell * (N - 1) + i] = o.T[i]; thr_s[i] = o.T[i]; }
-            a.max_level[cell] = o.max_level;
-            ml_s = o.max_level;
-            ok_s = o.status == SPROUT_CELL_OK;
+            const bool good = s0 >= 0 && s0 <= s1 && s1 <= a.n_requests && (s1 - s0) < (int64_t)0xFFFFFFFFll;
+            seg_ok_s = good;
+            if (!good) err |= SPROUT_TRACE_BAD_OFFSETS;
         }
-        for (int i = tid; i < NCM * N * 2; i += kClThreads) (&csum[0][0][0])[i] = 0ull;
+        for (int i = tid; i < kClMaxPieces * G * N; i += kClThreads) (&pcnt[0][0])[i] = 0u;
+        for (int i = tid; i < G * N; i += kClThreads) ctot[i] = 0u;
+        for (int i = tid; i < kClWarps * (NCELL + NSEG); i += kClThreads) (&part64[0][0])[i] = 0ull;
         __syncthreads();
-        const bool cell_ok = ok_s;
-        uint32_t T[N > 1 ? N - 1 : 1];
+        const bool seg_ok = seg_ok_s;
+        bool okc[G];
+        uint32_t T[G][N > 1 ? N - 1 : 1];
+        int ml[G];
 #pragma unroll
-        for (int i = 0; i + 1 < N; ++i) T[i] = thr_s[i];
-        const int ml = ml_s;
-        uint32_t cc[NCM][N], ct[NCM][N];
+        for (int c = 0; c < G; ++c) {
+            okc[c] = ok_s[c] != 0 && seg_ok;
+            ml[c] = ml_s[c];
 #pragma unroll
-        for (int c = 0; c < NCM; ++c)
+            for (int i = 0; i + 1 < N; ++i) T[c][i] = thr_s[c][i];
+        }
+        // pieces of kClPiece requests, 8-aligned in the local index (first_request % 8 == 0)
+        const int64_t pstart = seg_ok ? (s0 & ~(int64_t)7) : 0, pend = seg_ok ? s1 : 0;
+        const int n_pieces = pend > pstart ? (int)((pend - pstart + kClPiece - 1) / kClPiece) : 0;
+
+        // ---- pass 1: select every request in every chain; the interval's cell and
+        // segment sums in registers, per-piece level counts in shared memory ----
+        uint32_t cs[G][NCM][N], ts[G][NCM][N];
+        uint32_t sm[NCM][N + 2];
 #pragma unroll
-            for (int L = 0; L < N; ++L) { cc[c][L] = 0u; ct[c][L] = 0u; }
-        if (cell_ok) {
-            // Pieces of up to kClPiece requests, aligned on global quads (4 requests per Philox
-            // call).  Pass A: warp w takes a contiguous run of the piece's quads, 128 requests per
-            // step (lane l draws quad l of the step and hands the words out by shuffles), selects
-            // every request's level, accumulates the cell and stores (level, class, tokens) in
-            // shared memory, counting its level-L requests.  One barrier; then every warp knows
-            // how many level-L requests precede its run (request order), and pass B re-walks the
-            // run to write the last W of each level into the ring.
-            const uint64_t gs0 = a.first_request + (uint64_t)s0, gs1 = a.first_request + (uint64_t)s1;
-            const uint64_t q0 = gs0 >> 2, q1 = (gs1 + 3) >> 2;
-            for (uint64_t pq = q0; pq < q1; pq += kClPiece / 4) {
-                const uint64_t pq1 = min(q1, pq + kClPiece / 4);
-                const uint64_t nq = pq1 - pq;
-                const uint64_t per_w = ((nq + kClWarps * 32 - 1) / (kClWarps * 32)) * 32;   // quads per warp
-                const uint64_t wq0 = min(pq1, pq + per_w * warp), wq1 = min(pq1, wq0 + per_w);
-                int cntL[N];
-                int dn[N][NCM], dk[N][NCM];   // this lane's window deltas in the piece
+        for (int c = 0; c < G; ++c)
 #pragma unroll
-                for (int L = 0; L < N; ++L) {
-                    cntL[L] = 0;
+            for (int cc = 0; cc < NCM; ++cc)
 #pragma unroll
-                    for (int c = 0; c < NCM; ++c) { dn[L][c] = 0; dk[L][c] = 0; }
-                }
-                for (uint64_t qb = wq0; qb < wq1; qb += 32) {
-                    // the block's tokens at every level and its flags are loaded first (independent,
-                    // coalesced loads in flight together; the level only selects among them)
-                    uint32_t tk4[4][N], fb4[4];
+                for (int L = 0; L < N; ++L) { cs[c][cc][L] = 0u; ts[c][cc][L] = 0u; }
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint64_t g = qb * 4 + 32 * k + lane;
-                        const bool ld = g >= gs0 && g < gs1;
-                        const int64_t rq = (int64_t)(g - a.first_request);
+        for (int cc = 0; cc < NCM; ++cc)
 #pragma unroll
-                        for (int L = 0; L < N; ++L) tk4[k][L] = ld ? (uint32_t)__ldcs(a.tokens + (size_t)L * a.pitch + rq) : 0u;
-                        fb4[k] = (ld && a.flags) ? (uint32_t)__ldcs(a.flags + rq) : 0u;
-                    }
-                    const uint64_t myq = qb + lane;
-                    Philox4 d = philox4x32_10_rk((uint32_t)myq, (uint32_t)(myq >> 32), 0u, 0u, a.rk0, a.rk1);
+            for (int f = 0; f < N + 2; ++f) sm[cc][f] = 0u;
+        // 32-bit sums per thread are folded into part64 every 32 pieces (<= 256 requests per thread)
+        auto flush = [&]() {
+            int v = 0;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int src = 8 * k + (lane >> 2);
-                        const uint32_t v0 = __shfl_sync(0xFFFFFFFFu, d.v[0], src);
-                        const uint32_t v1 = __shfl_sync(0xFFFFFFFFu, d.v[1], src);
-                        const uint32_t v2 = __shfl_sync(0xFFFFFFFFu, d.v[2], src);
-                        const uint32_t v3 = __shfl_sync(0xFFFFFFFFu, d.v[3], src);
-                        const uint32_t sel = lane & 3u;
-                        const uint32_t w = sel == 0 ? v0 : sel == 1 ? v1 : sel == 2 ? v2 : v3;
-                        const uint64_t g = qb * 4 + 32 * k + lane;
-                        const bool qin = qb + (uint64_t)(8 * k + (lane >> 2)) < wq1;   // quad of this warp
-                        const bool inr = qin && g >= gs0 && g < gs1;
-                        const int64_t rq = (int64_t)(g - a.first_request);
-                        int lev = -1;
-                        uint32_t cls = 0u, tl = 0u;
-                        if (inr) {
-                            const uint32_t pin = fb4[k] & 1u;
-                            cls = (fb4[k] >> 1) & 3u;
-                            if (cls >= (uint32_t)NC) {
-                                err |= SPROUT_TRACE_BAD_CLASS;
-                            } else {
-                                int L = 0;
+            for (int c = 0; c < G; ++c)
 #pragma unroll
-                                for (int i = 0; i + 1 < N; ++i) L += (w >= T[i]) ? 1 : 0;
-                                L = pin ? 0 : min(L, ml);
-                                lev = L;
-                                tl = tk4[k][0];
-#pragma unroll
-                                for (int LL = 1; LL < N; ++LL) tl = L == LL ? tk4[k][LL] : tl;
-#pragma unroll
-                                for (int c = 0; c < NCM; ++c)
-#pragma unroll
-                                    for (int LL = 0; LL < N; ++LL) {
-                                        const bool hit = (uint32_t)c == cls && LL == L;
-                                        cc[c][LL] += hit ? 1u : 0u;
-                                        ct[c][LL] += hit ? tl : 0u;
-                                    }
-                            }
-                        }
-                        const uint64_t pos = (qb - pq) * 4 + 32 * k + lane;   // piece-relative slot
-                        if (qin) buf[pos] = lev < 0 ? 0xFF000000u : ((uint32_t)lev << 24) | (cls << 16) | tl;
-#pragma unroll
-                        for (int L = 0; L < N; ++L) cntL[L] += __popc(__ballot_sync(0xFFFFFFFFu, lev == L));
-                    }
-                }
-                if (lane < N) {
-                    int v = cntL[0];
-#pragma unroll
-                    for (int L = 1; L < N; ++L) v = lane == L ? cntL[L] : v;
-                    wcount[warp][lane] = v;
-                }
-                __syncthreads();
-                int before[N], total[N];
-#pragma unroll
-                for (int L = 0; L < N; ++L) {
-                    before[L] = 0;
-                    total[L] = 0;
-                    for (int w2 = 0; w2 < kClWarps; ++w2) {
-                        before[L] += w2 < warp ? wcount[w2][L] : 0;
-                        total[L] += wcount[w2][L];
-                    }
-                }
-                // only the last W requests of each level in the piece enter the ring: a warp
-                // whose run ends before them has nothing to write
-                bool any = false;
-#pragma unroll
-                for (int L = 0; L < N; ++L) {
-                    int mine = 0;
-                    for (int w2 = 0; w2 < kClWarps; ++w2) mine += w2 == warp ? wcount[w2][L] : 0;
-                    any = any || (before[L] + mine > total[L] - W && mine > 0);
-                }
-                for (uint64_t qb = wq0; any && qb < wq1; qb += 32) {
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint64_t pos = (qb - pq) * 4 + 32 * k + lane;
-                        const bool qin = qb + (uint64_t)(8 * k + (lane >> 2)) < wq1;
-                        const uint32_t v = qin ? buf[pos] : 0xFF000000u;
-                        const int lev = (int)(v >> 24);
-#pragma unroll
-                        for (int L = 0; L < N; ++L) {
-                            const uint32_t bl = __ballot_sync(0xFFFFFFFFu, lev == L);
-                            if (lev == L) {
-                                const int rank = before[L] + __popc(bl & ((1u << lane) - 1u));
-                                if (rank >= total[L] - W) {
-                                    // the slot's previous entry (from before this piece) leaves the
-                                    // window: occupied iff the ring was full or the slot is below its fill
-                                    const int slot = (int)(((int64_t)head[L] + rank) % W);
-                                    if (size[L] == W || slot < size[L]) {
-                                        const uint32_t old = ring[L * W + slot];
-                                        const int oc = (int)(old >> 16);
-#pragma unroll
-                                        for (int c = 0; c < NCM; ++c)
-                                            if (c == oc) { dn[L][c] -= 1; dk[L][c] -= (int)(old & 0xFFFFu); }
-                                    }
-                                    ring[L * W + slot] = v & 0x00FFFFFFu;
-#pragma unroll
-                                    for (int c = 0; c < NCM; ++c)
-                                        if ((uint32_t)c == ((v >> 16) & 0xFFu)) { dn[L][c] += 1; dk[L][c] += (int)(v & 0xFFFFu); }
-                                }
-                            }
-                            before[L] += __popc(bl);
-                        }
-                    }
-                }
-                // fold the piece: per-warp sums into slots, then one thread per value adds the
-                // 8 warps (no shared atomics; every sum is an exact integer)
-#pragma unroll
-                for (int c = 0; c < NCM; ++c) {
-                    if (c >= NC) break;
+                for (int cc = 0; cc < NCM; ++cc)
 #pragma unroll
                     for (int L = 0; L < N; ++L) {
-                        const uint32_t sc = __reduce_add_sync(0xFFFFFFFFu, cc[c][L]);
-                        const uint32_t st = __reduce_add_sync(0xFFFFFFFFu, ct[c][L]);
-                        const int sn = (int)__reduce_add_sync(0xFFFFFFFFu, (uint32_t)dn[L][c]);
-                        const int sk = (int)__reduce_add_sync(0xFFFFFFFFu, (uint32_t)dk[L][c]);
-                        if (lane == 0) {
-                            const int v = (c * N + L) * 4;
-                            slots[warp][v + 0] = sc; slots[warp][v + 1] = st;
-                            slots[warp][v + 2] = (uint32_t)sn; slots[warp][v + 3] = (uint32_t)sk;
-                        }
-                        cc[c][L] = 0u; ct[c][L] = 0u;
+                        const uint32_t x0 = __reduce_add_sync(0xFFFFFFFFu, cs[c][cc][L]);
+                        const uint32_t x1 = __reduce_add_sync(0xFFFFFFFFu, ts[c][cc][L]);
+                        if (lane == 0) { part64[warp][v] += x0; part64[warp][v + 1] += x1; }
+                        v += 2;
+                        cs[c][cc][L] = 0u; ts[c][cc][L] = 0u;
                     }
-                }
-                __syncthreads();
-                if (tid < N) {
-                    int tt = total[0];
 #pragma unroll
-                    for (int L = 1; L < N; ++L) tt = tid == L ? total[L] : tt;
-                    head[tid] = (int)(((int64_t)head[tid] + tt) % W);
-                    size[tid] = min(size[tid] + tt, W);
+            for (int cc = 0; cc < NCM; ++cc)
+#pragma unroll
+                for (int f = 0; f < N + 2; ++f) {
+                    const uint32_t x = __reduce_add_sync(0xFFFFFFFFu, sm[cc][f]);
+                    if (lane == 0) part64[warp][NCELL + cc * (N + 2) + f] += x;
+                    sm[cc][f] = 0u;
                 }
-                for (int v = tid; v < NC * N; v += kClThreads) {
-                    const int c = v / N, L = v % N;
-                    unsigned long long sc = 0, st = 0;
-                    long long sn = 0, sk = 0;
-                    for (int w2 = 0; w2 < kClWarps; ++w2) {
-                        sc += slots[w2][v * 4 + 0]; st += slots[w2][v * 4 + 1];
-                        sn += (int)slots[w2][v * 4 + 2]; sk += (int)slots[w2][v * 4 + 3];
+        };
+        for (int pi = 0; pi < n_pieces; ++pi) {
+            if (pi > 0 && (pi & 31) == 0) flush();
+            prefetch_piece<N>(a, pstart + (int64_t)(pi + 2) * kClPiece, pend, tid);
+            const int64_t c0 = pstart + (int64_t)pi * kClPiece + 8 * (int64_t)tid;
+            const bool any = c0 + 8 > s0 && c0 < s1;
+            Chunk<N> ch;
+            load_chunk<N>(a, c0, any, ch);
+            uint32_t lc[G][N];
+#pragma unroll
+            for (int c = 0; c < G; ++c)
+#pragma unroll
+                for (int L = 0; L < N; ++L) lc[c][L] = 0u;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int64_t g = c0 + k;
+                const uint32_t fb = flag_byte(ch.fw, k);
+                const uint32_t cls = (fb >> 1) & 3u;
+                const bool pinned = fb & 1u;
+                const bool inr = any && g >= s0 && g < s1;
+                if (inr && cls >= (uint32_t)NC) err |= SPROUT_TRACE_BAD_CLASS;
+                if (!(inr && cls < (uint32_t)NC)) continue;
+                uint32_t tl[N];
+#pragma unroll
+                for (int L = 0; L < N; ++L) tl[L] = cl_half(ch.tk[L], k);
+                if (seg_writer) {
+#pragma unroll
+                    for (int cc = 0; cc < NCM; ++cc) {
+                        if ((uint32_t)cc != cls) continue;
+                        sm[cc][0] += 1u;
+                        sm[cc][1] += pinned ? 1u : 0u;
+#pragma unroll
+                        for (int L = 0; L < N; ++L) sm[cc][2 + L] += tl[L];
                     }
-                    csum[c][L][0] += sc; csum[c][L][1] += st;
-                    wsum[L][c][0] = (unsigned long long)((long long)wsum[L][c][0] + sn);
-                    wsum[L][c][1] = (unsigned long long)((long long)wsum[L][c][1] + sk);
                 }
-                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < G; ++c) {
+                    if (!okc[c]) continue;
+                    const int L = cl_level<N>(ch.w[k], T[c], ml[c], pinned);
+#pragma unroll
+                    for (int LL = 0; LL < N; ++LL) {
+                        const bool hit = LL == L;
+                        lc[c][LL] += hit ? 1u : 0u;
+#pragma unroll
+                        for (int cc = 0; cc < NCM; ++cc) {
+                            const bool h2 = hit && (uint32_t)cc == cls;
+                            cs[c][cc][LL] += h2 ? 1u : 0u;
+                            ts[c][cc][LL] += h2 ? tl[LL] : 0u;
+                        }
+                    }
+                }
             }
-        }
-        __syncthreads();
-        if (tid == 0) {   // cell_epilogue's formulas and order
-            const double kp = k0_s * a.pue;
-            double E = 0.0, Tm = 0.0, Q = 0.0;
-            for (int c = 0; c < NC; ++c) {
+#pragma unroll
+            for (int c = 0; c < G; ++c)
 #pragma unroll
                 for (int L = 0; L < N; ++L) {
-                    const unsigned long long cn = cell_ok ? csum[c][L][0] : 0ull, tk = cell_ok ? csum[c][L][1] : 0ull;
-                    a.cnt[(cell * NC + c) * N + L] = cn;
-                    a.tok[(cell * NC + c) * N + L] = tk;
-                    const double n_ = (double)cn, t_ = (double)tk;
-                    E += n_ * cost.ef[c][L] + t_ * cost.et[c][L];
-                    Tm += n_ * cost.pf[c][L] + t_ * cost.pt[c][L];
-                    Q += n_ * q_r[L];
+                    const uint32_t v = __reduce_add_sync(0xFFFFFFFFu, lc[c][L]);
+                    if (lane == 0 && v) {
+                        atomicAdd(&ctot[c * N + L], v);
+                        if (pi < kClMaxPieces) atomicAdd(&pcnt[pi][c * N + L], v);
+                    }
+                }
+        }
+        flush();
+        __syncthreads();
+        // interval totals per (chain, level) and the first piece holding one of the
+        // last W requests (the ones that enter the window); pcnt becomes the level-L
+        // requests BEFORE each piece
+        const bool long_interval = n_pieces > kClMaxPieces;   // (> 2^20 requests: counts re-derived below)
+        if (tid < G * N) {
+            const uint32_t tot = ctot[tid];
+            uint32_t run0 = 0u;
+            for (int pi = 0; pi < n_pieces && pi < kClMaxPieces; ++pi) { const uint32_t v = pcnt[pi][tid]; pcnt[pi][tid] = run0; run0 += v; }
+            uint32_t first = 0u;
+            if (!long_interval) {   // the first piece whose level-L requests reach the window (index >= tot - W)
+                const uint32_t need = tot > (uint32_t)W ? tot - (uint32_t)W : 0u;
+                first = (uint32_t)n_pieces;
+                for (int pi = n_pieces - 1; pi >= 0; --pi) {
+                    const uint32_t next = pi + 1 < n_pieces ? pcnt[pi + 1][tid] : tot;
+                    if (next > need) first = (uint32_t)pi; else break;
+                }
+            }
+            cfirst[tid] = first;
+        }
+        __syncthreads();
+        // ---- pass 2: the window entries, in request order (a block scan per piece
+        // gives every request its forward index among its (chain, level)) ----
+        int dn[G][N][NCM], dk[G][N][NCM];
+#pragma unroll
+        for (int c = 0; c < G; ++c)
+#pragma unroll
+            for (int L = 0; L < N; ++L)
+#pragma unroll
+                for (int cc = 0; cc < NCM; ++cc) { dn[c][L][cc] = 0; dk[c][L][cc] = 0; }
+        int p_first = n_pieces;
+        uint32_t tot_c[G][N];
+#pragma unroll
+        for (int c = 0; c < G; ++c)
+#pragma unroll
+            for (int L = 0; L < N; ++L) {
+                tot_c[c][L] = ctot[c * N + L];
+                if (okc[c] && tot_c[c][L] > 0u) p_first = min(p_first, long_interval ? 0 : (int)cfirst[c * N + L]);
+            }
+        uint32_t run[G][N];   // long intervals: level-L requests of the pieces already walked
+#pragma unroll
+        for (int c = 0; c < G; ++c)
+#pragma unroll
+            for (int L = 0; L < N; ++L) run[c][L] = 0u;
+        const int p2 = long_interval ? 0 : p_first;
+        prefetch_piece<N>(a, pstart + (int64_t)p2 * kClPiece, pend, tid);
+        for (int pi = p2; pi < n_pieces; ++pi) {
+            prefetch_piece<N>(a, pstart + (int64_t)(pi + 1) * kClPiece, pend, tid);
+            const int64_t c0 = pstart + (int64_t)pi * kClPiece + 8 * (int64_t)tid;
+            const bool any = c0 + 8 > s0 && c0 < s1;
+            Chunk<N> ch;
+            load_chunk<N>(a, c0, any, ch);
+            uint32_t lv[G];     // 2-bit... levels of the 8 requests per chain, 4 bits each
+            uint32_t lc[G][N];
+            uint32_t valid = 0u;
+#pragma unroll
+            for (int c = 0; c < G; ++c) {
+                lv[c] = 0u;
+#pragma unroll
+                for (int L = 0; L < N; ++L) lc[c][L] = 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int64_t g = c0 + k;
+                const uint32_t fb = flag_byte(ch.fw, k);
+                const bool v = any && g >= s0 && g < s1 && ((fb >> 1) & 3u) < (uint32_t)NC;
+                valid |= v ? (1u << k) : 0u;
+                if (!v) continue;
+#pragma unroll
+                for (int c = 0; c < G; ++c) {
+                    const int L = cl_level<N>(ch.w[k], T[c], ml[c], fb & 1u);
+                    lv[c] |= (uint32_t)L << (4 * k);
+#pragma unroll
+                    for (int LL = 0; LL < N; ++LL) lc[c][LL] += LL == L ? 1u : 0u;
+                }
+            }
+            // exclusive scan of the counts over the piece's threads
+            uint32_t before[G][N];
+#pragma unroll
+            for (int c = 0; c < G; ++c)
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    uint32_t x = lc[c][L];
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+                        if (lane >= d) x += y;
+                    }
+                    before[c][L] = x - lc[c][L];
+                    if (lane == 31) wtot[warp][c * N + L] = x;
+                }
+            __syncthreads();
+#pragma unroll
+            for (int c = 0; c < G; ++c)
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    uint32_t b = 0u, pt = 0u;
+                    for (int w2 = 0; w2 < kClWarps; ++w2) {
+                        const uint32_t v = wtot[w2][c * N + L];
+                        b += w2 < warp ? v : 0u;
+                        pt += v;
+                    }
+                    const uint32_t base = long_interval ? run[c][L] : pcnt[pi][c * N + L];
+                    before[c][L] += base + b;
+                    run[c][L] += pt;
+                }
+            __syncthreads();   // wtot is reused by the next piece
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                if (!((valid >> k) & 1u)) continue;
+                const uint32_t cls = (flag_byte(ch.fw, k) >> 1) & 3u;
+#pragma unroll
+                for (int c = 0; c < G; ++c) {
+                    if (!okc[c]) continue;
+                    const int L = (int)((lv[c] >> (4 * k)) & 15u);
+                    uint32_t idx = 0u, tot = 0u, tl = 0u;
+#pragma unroll
+                    for (int LL = 0; LL < N; ++LL)
+                        if (LL == L) { idx = before[c][LL]; tot = tot_c[c][LL]; tl = cl_half(ch.tk[LL], k); before[c][LL] += 1u; }
+                    if (idx + (uint32_t)W < tot) continue;   // not among the interval's last W of its level
+                    // forward index idx goes to slot head + idx (FIFO); the slot's entry from
+                    // before the interval leaves the window
+                    const int slot = (int)(((uint32_t)head[c][L] + idx) % (uint32_t)W);
+                    uint32_t *rp = ring + ((size_t)c * N + L) * W + slot;
+                    if (size[c][L] == W || slot < size[c][L]) {
+                        const uint32_t old = *rp;
+                        const uint32_t oc = old >> 16;
+#pragma unroll
+                        for (int LL = 0; LL < N; ++LL)
+#pragma unroll
+                            for (int cc = 0; cc < NCM; ++cc)
+                                if (LL == L && (uint32_t)cc == oc) { dn[c][LL][cc] -= 1; dk[c][LL][cc] -= (int)(old & 0xFFFFu); }
+                    }
+                    *rp = (cls << 16) | tl;
+#pragma unroll
+                    for (int LL = 0; LL < N; ++LL)
+#pragma unroll
+                        for (int cc = 0; cc < NCM; ++cc)
+                            if (LL == L && (uint32_t)cc == cls) { dn[c][LL][cc] += 1; dk[c][LL][cc] += (int)tl; }
+                }
+            }
+        }
+        if (t + 1 < a.T) {   // the next interval's first two pieces into L2 while this one is folded
+            const int64_t n0 = a.seg_offsets[sl + 1], n1 = a.seg_offsets[sl + 2];
+            if (n0 >= 0 && n0 <= n1 && n1 <= a.n_requests) {
+                prefetch_piece<N>(a, n0 & ~(int64_t)7, n1, tid);
+                prefetch_piece<N>(a, (n0 & ~(int64_t)7) + kClPiece, n1, tid);
+            }
+        }
+        // ---- fold the interval: window deltas per warp, then one thread per value ----
+        {
+            int v = 0;
+#pragma unroll
+            for (int c = 0; c < G; ++c)
+#pragma unroll
+                for (int L = 0; L < N; ++L)
+#pragma unroll
+                    for (int cc = 0; cc < NCM; ++cc) {
+                        const uint32_t x0 = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)dn[c][L][cc]);
+                        const uint32_t x1 = __reduce_add_sync(0xFFFFFFFFu, (uint32_t)dk[c][L][cc]);
+                        if (lane == 0) { part[warp][v] = x0; part[warp][v + 1] = x1; }
+                        v += 2;
+                    }
+        }
+        __syncthreads();
+        __shared__ unsigned long long tot64[NCELL + NSEG];
+        for (int v = tid; v < NDELTA; v += kClThreads) {
+            long long sum = 0;
+            for (int w2 = 0; w2 < kClWarps; ++w2) sum += (long long)(int)part[w2][v];
+            unsigned long long *wp = &wsum[0][0][0][0] + v;
+            *wp = (unsigned long long)((long long)*wp + sum);
+        }
+        for (int v = tid; v < NCELL + NSEG; v += kClThreads) {
+            unsigned long long sum = 0ull;
+            for (int w2 = 0; w2 < kClWarps; ++w2) sum += part64[w2][v];
+            tot64[v] = sum;
+        }
+        if (tid < G * N) {
+            const int c = tid / N, L = tid % N;
+            const uint32_t tt = okc[c] ? ctot[tid] : 0u;
+            head[c][L] = (int)(((uint32_t)head[c][L] + tt) % (uint32_t)W);
+            size[c][L] = (int)min((uint32_t)size[c][L] + tt, (uint32_t)W);
+        }
+        __syncthreads();
+        // ---- the interval's outputs: G cells (cell_epilogue's formulas and order) and the segment ----
+        const double kp = __dmul_rn(k0_s, a.pue);
+        if (tid < G && j0 + tid < a.X) {
+            const int c = tid;
+            const int64_t cell = sl * a.X + j0 + c;
+            const bool okk = ok_s[c] != 0 && seg_ok;
+            double E = 0.0, Tm = 0.0, Q = 0.0;
+            for (int cc = 0; cc < NC; ++cc) {
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    const int v = ((c * NCM + cc) * N + L) * 2;
+                    const unsigned long long cn = okk ? tot64[v] : 0ull, tk2 = okk ? tot64[v + 1] : 0ull;
+                    a.cnt[(cell * NC + cc) * N + L] = cn;
+                    a.tok[(cell * NC + cc) * N + L] = tk2;
+                    const double n_ = (double)cn, t_ = (double)tk2;
+                    E += n_ * cost.ef[cc][L] + t_ * cost.et[cc][L];
+                    Tm += n_ * cost.pf[cc][L] + t_ * cost.pt[cc][L];
+                    Q += n_ * qrow[L];
                 }
             }
             a.energy[cell] = E;
             a.time_s[cell] = Tm;
-            a.carbon[cell] = cell_ok ? kp * E + a.k1 * Tm : 0.0;
+            a.carbon[cell] = okk ? kp * E + a.k1 * Tm : 0.0;
             a.quality[cell] = Q;
+        }
+        if (seg_writer && tid == G) {   // write_seg_stats' formulas and order (trace_sim.cu)
+            const unsigned long long *ss = tot64 + NCELL;   // [NCM][N + 2]
+            double bE = 0.0, bT = 0.0, m = 0.0;
+            for (int cc = 0; cc < NC; ++cc) {
+                const unsigned long long mc = ss[cc * (N + 2)];
+                a.seg_count[sl * NC + cc] = mc;
+                a.seg_pinned[sl * NC + cc] = ss[cc * (N + 2) + 1];
+                for (int L = 0; L < N; ++L) a.seg_tok[(sl * NC + cc) * N + L] = ss[cc * (N + 2) + 2 + L];
+                bE += (double)mc * cost.ef[cc][0] + (double)ss[cc * (N + 2) + 2] * cost.et[cc][0];
+                bT += (double)mc * cost.pf[cc][0] + (double)ss[cc * (N + 2) + 2] * cost.pt[cc][0];
+                m += (double)mc;
+            }
+            a.seg_base[sl * 4 + 0] = bE;
+            a.seg_base[sl * 4 + 1] = bT;
+            a.seg_base[sl * 4 + 2] = kp * bE + a.k1 * bT;
+            a.seg_base[sl * 4 + 3] = m * qrow[0];
         }
         __syncthreads();
     }
@@ -334,24 +530,50 @@ __global__ void __launch_bounds__(kClThreads) closed_loop_kernel(const __grid_co
     if (lane == 0 && err) atomicOr(a.trace_status, err);
 }
 
-cudaError_t launch_closed_loop(const ClosedArgs &a, cudaStream_t stream, int *launches) {
-    const int64_t chains = (int64_t)a.R_local * a.X;
-    if (chains == 0) return cudaSuccess;
-    const size_t smem = ((size_t)a.n * a.W + kClPiece) * 4;
+// chains per CTA: the smallest group that keeps every region's groups on
+// distinct SMs (a CTA per SM; more chains per CTA only add per-request work),
+// at most kMaxG, one chain per CTA with several classes (the per-thread sums),
+// and the group's rings within shared memory
+constexpr int kMaxG = 4;
+static int pick_group(const ClosedArgs &a, int sms) {
+    if (a.NC > 1) return 1;
+    int G = 1;
+    while (G < kMaxG && (int64_t)a.R_local * ((a.X + G - 1) / G) > sms && (size_t)(G + 1) * a.n * a.W * 4 <= 160 * 1024)
+        ++G;
+    return G;
+}
+
+cudaError_t launch_closed_loop(ClosedArgs &a, cudaStream_t stream, int *launches) {
+    if ((int64_t)a.R_local * a.X == 0) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int G = pick_group(a, sms);
+    a.n_groups = (a.X + G - 1) / G;
+    const int64_t blocks = (int64_t)a.R_local * a.n_groups;
+    const size_t smem = (size_t)G * a.n * a.W * 4;
     cudaError_t e = cudaSuccess;
-#define CL_CASE(NN)                                                                                  \
-    case NN: {                                                                                       \
-        auto kern = a.NC == 1 ? closed_loop_kernel<NN, 1> : closed_loop_kernel<NN, kMaxClasses>;     \
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
-        if (e != cudaSuccess) return e;                                                              \
-        kern<<<(unsigned)chains, kClThreads, smem, stream>>>(a);                                     \
-        break;                                                                                       \
+#define CL_LAUNCH(NN, NCM_, GG)                                                                   \
+    {                                                                                             \
+        auto kern = closed_loop_kernel<NN, NCM_, GG>;                                             \
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
+        if (e != cudaSuccess) return e;                                                           \
+        kern<<<(unsigned)blocks, kClThreads, smem, stream>>>(a);                                  \
     }
+#define CL_G(NN)                                                                                  \
+    case NN:                                                                                      \
+        if (a.NC > 1) CL_LAUNCH(NN, kMaxClasses, 1)                                               \
+        else if (G == 1) CL_LAUNCH(NN, 1, 1)                                                      \
+        else if (G == 2) CL_LAUNCH(NN, 1, 2)                                                      \
+        else if (G == 3) CL_LAUNCH(NN, 1, 3)                                                      \
+        else CL_LAUNCH(NN, 1, 4)                                                                  \
+        break;
     switch (a.n) {
-        CL_CASE(1) CL_CASE(2) CL_CASE(3) CL_CASE(4) CL_CASE(5) CL_CASE(6) CL_CASE(7) CL_CASE(8)
+        CL_G(1) CL_G(2) CL_G(3) CL_G(4) CL_G(5) CL_G(6) CL_G(7) CL_G(8)
         default: return cudaErrorInvalidValue;
     }
-#undef CL_CASE
+#undef CL_G
+#undef CL_LAUNCH
     ++*launches;
     return cudaGetLastError();
 }

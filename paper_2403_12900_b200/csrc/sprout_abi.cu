@@ -209,7 +209,8 @@ sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int3
     if (st == SPROUT_OK) st = validate_trace(problem, trace);
     if (st == SPROUT_OK) st = validate_cost(cost);
     if (st != SPROUT_OK) return st;
-    if (!totals || !totals->trace_status) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (st == SPROUT_OK) st = validate_totals(problem, totals);
+    if (st != SPROUT_OK) return st;
     // whole regions only: a chain is one region's intervals in order
     if (problem->first_segment % problem->n_intervals != 0 || problem->n_segments % problem->n_intervals != 0 ||
         problem->profile_per_interval != 0)
@@ -217,14 +218,12 @@ sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int3
     const int64_t S = problem->n_segments;
     if (window < 1 || window > 4096 || (int64_t)problem->n_levels * window * 4 > 192 * 1024)
         return SPROUT_ERR_INVALID_ARGUMENT;
-    if (S > 0 && (!totals->cnt || !totals->tok || !totals->energy_kwh || !totals->time_s || !totals->carbon_g ||
-                  !totals->quality))
-        return SPROUT_ERR_INVALID_ARGUMENT;
     if (profile_out && !aligned(profile_out, 8)) return SPROUT_ERR_INVALID_ARGUMENT;
     ClosedArgs a{};
     a.n = problem->n_levels; a.R = problem->n_regions; a.X = problem->n_xi; a.NC = cost->n_classes; a.W = window;
     a.T = problem->n_intervals;
     a.first_segment = problem->first_segment;
+    a.n_requests = trace->n_requests;
     a.r0 = (int)(problem->first_segment / problem->n_intervals);
     a.R_local = (int)(problem->n_segments / problem->n_intervals);
     a.k0 = problem->k0; a.kmin = problem->k0_min; a.kmax = problem->k0_max; a.xi = problem->xi;
@@ -244,6 +243,8 @@ sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int3
     a.threshold = solution->threshold;
     a.cnt = totals->cnt; a.tok = totals->tok; a.energy = totals->energy_kwh; a.time_s = totals->time_s;
     a.carbon = totals->carbon_g; a.quality = totals->quality; a.trace_status = totals->trace_status;
+    a.seg_count = totals->seg_count; a.seg_pinned = totals->seg_pinned; a.seg_tok = totals->seg_tok;
+    a.seg_base = totals->seg_base;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (cudaMemsetAsync(totals->trace_status, 0, 4, s) != cudaSuccess) return SPROUT_ERR_CUDA;
     int launches = 0;

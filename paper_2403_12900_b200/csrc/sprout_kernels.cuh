@@ -56,8 +56,10 @@ struct LpArgs {
 struct ClosedArgs {             // closed-loop profiles (closed_loop.cu)
     int n, R, X, NC, W;
     int r0, R_local;           // regions [r0, r0 + R_local) of this call (whole regions)
-    int64_t T, first_segment;
+    int n_groups;              // CTAs per region: chain groups of G xi values (set by the launcher)
+    int64_t T, first_segment, n_requests;
     const double *k0, *kmin, *kmax, *xi, *e, *p, *q;   // e, p: priors [R][n]
+    const double *q_seg;       // NULL or [R*T][n]: q per interval (evaluation epochs), else q[R][n]
     double k1, pue;
     uint32_t rk0[10], rk1[10];
     CostConst cost;
@@ -71,6 +73,8 @@ struct ClosedArgs {             // closed-loop profiles (closed_loop.cu)
     uint32_t *threshold;
     uint64_t *cnt, *tok;
     double *energy, *time_s, *carbon, *quality;
+    uint64_t *seg_count, *seg_pinned, *seg_tok;
+    double *seg_base;
     uint32_t *trace_status;
 };
 
@@ -185,7 +189,7 @@ size_t reduce_workspace_bytes(int n, int X, int R, int64_t T, int64_t first_segm
 cudaError_t launch_reduce(ReduceArgs &a, void *ws, cudaStream_t stream, int *launches);
 cudaError_t launch_generate(const GenArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_evaluator(const EvalArgs &a, cudaStream_t stream, int *launches);
-cudaError_t launch_closed_loop(const ClosedArgs &a, cudaStream_t stream, int *launches);
+cudaError_t launch_closed_loop(ClosedArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_select_static(const SelectArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_check_cells(const uint8_t *status, int64_t n_cells, uint32_t *out, cudaStream_t stream, int *launches);
 

@@ -101,7 +101,8 @@ class Sweep:
 
     def closed_loop(self, window: int, profile: bool = False, stream=None):
         """Closed-loop profiles (NEXT-1): steps 1-2 as a causal scan per
-        (region, xi) chain; the segment statistics come from simulate()."""
+        (region, xi) chain; writes the solution and every totals field
+        (cells and segments), so reduce() can follow directly."""
         prof = None
         if profile:
             prof = torch.zeros((self.dp.cells, 2, self.prob_host.n), dtype=torch.float64, device=self.device)

@@ -253,8 +253,8 @@ class Totals:
     @classmethod
     def empty(cls, prob: DeviceProblem, n_classes: int) -> "Totals":
         dev, cells, n, S = prob.k0.device, prob.cells, prob.n, prob.n_segments
-        i64 = lambda *s: torch.empty(s, dtype=torch.int64, device=dev)
-        f64 = lambda *s: torch.empty(s, dtype=torch.float64, device=dev)
+        i64 = lambda *s: torch.zeros(s, dtype=torch.int64, device=dev)
+        f64 = lambda *s: torch.zeros(s, dtype=torch.float64, device=dev)
         return cls(i64(cells, n_classes, n), i64(cells, n_classes, n), f64(cells), f64(cells), f64(cells),
                    f64(cells), i64(S, n_classes), i64(S, n_classes), i64(S, n_classes, n), f64(S, 4),
                    torch.zeros(1, dtype=torch.int32, device=dev))

@@ -66,3 +66,69 @@ def test_closed_loop_region_shards(world):
         np.testing.assert_array_equal(got["cnt"].reshape(-1, NC, n), want["cnt"][lo:hi])
         np.testing.assert_array_equal(got["tok"].reshape(-1, NC, n), want["tok"][lo:hi])
         np.testing.assert_allclose(got["carbon"].reshape(-1), want["carbon"][lo:hi], rtol=FP_RTOL, atol=0)
+
+
+@pytest.mark.parametrize("name,kw,W", [("C2", dict(n_requests=60_000, n_intervals=48), 200),
+                                       ("C3", dict(n_requests=30_000, n_intervals=72, n_regions=2), 50),
+                                       ("C4", dict(n_requests=120_000, n_intervals=24, n_regions=2), 1000)])
+def test_closed_loop_then_reduce(name, kw, W):
+    """The closed-loop step alone gives complete totals:
+    segment statistics and the Base counterfactual equal the open-loop
+    oracle's (they do not depend on the scheme), and reduce() over the
+    closed-loop cells equals oracle.reduce over the oracle's closed-loop cells."""
+    w = synth.make_workload(name, **kw)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, fl = synth.host_trace(w.spec, sh)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=fl)
+    sw.closed_loop(W)
+    sw.reduce()
+    torch.cuda.synchronize()
+    got = sw.host()
+    cl = oracle.closed_loop(w.prob, w.cost, W, w.spec.seg_offsets, toks, fl)
+    S_ = w.prob.R * w.prob.T
+    off = w.spec.seg_offsets
+    sim = oracle.simulate(w.prob, w.cost, np.arange(S_), off[:-1], np.diff(off), off[:-1], toks, fl)
+    np.testing.assert_array_equal(got["seg_count"].reshape(sim["seg_count"].shape), sim["seg_count"])
+    np.testing.assert_array_equal(got["seg_pinned"].reshape(sim["seg_pinned"].shape), sim["seg_pinned"])
+    np.testing.assert_array_equal(got["seg_tok"].reshape(sim["seg_tok"].shape), sim["seg_tok"])
+    np.testing.assert_allclose(got["seg_base"].reshape(sim["seg_base"].shape), sim["seg_base"], rtol=FP_RTOL, atol=0)
+    np.testing.assert_array_equal(got["objective"].view(np.uint64), cl["objective"].view(np.uint64))
+    X, NC, n = w.prob.X, w.cost.n_classes, w.prob.n
+    cells = dict(cell_status=cl["cell_status"], objective=cl["objective"])
+    simc = dict(cnt=cl["cnt"].reshape(S_, X, NC, n), tok=cl["tok"].reshape(S_, X, NC, n),
+                energy=cl["energy"].reshape(S_, X), time=cl["time"].reshape(S_, X),
+                carbon=cl["carbon"].reshape(S_, X), quality=cl["quality"].reshape(S_, X),
+                seg_count=sim["seg_count"], seg_pinned=sim["seg_pinned"], seg_base=sim["seg_base"])
+    simc = {k: np.ascontiguousarray(v) for k, v in simc.items()}
+    G = oracle.reduce(w.prob, NC, 0, S_, cells, simc)
+    np.testing.assert_allclose(got["group"], G, rtol=FP_RTOL, atol=0)
+    assert got["group"][-1, 0, 0] == w.N   # every request counted (group stat 0)
+    assert got["trace_status"] == 0
+
+
+def test_closed_loop_bad_offsets():
+    """Invalid offsets are flagged and the interval skipped: its
+    cells and segment fields are zero and nothing enters the windows, as in
+    sprout_simulate_trace."""
+    w = synth.make_workload("C2", n_requests=20_000, n_intervals=24)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, fl = synth.host_trace(w.spec, sh)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=fl)
+    bad = sh.seg_offsets.copy()
+    T = w.prob.T
+    bad[5] = sh.n_requests + 100    # segment 4 ends past the trace, segment 5 starts there
+    sw.trace.seg_offsets.copy_(torch.as_tensor(bad))
+    sw.closed_loop(50)
+    sw.reduce()
+    torch.cuda.synchronize()
+    got = sw.host()
+    assert got["trace_status"] & S.TRACE_BAD_OFFSETS
+    X, NC, n = w.prob.X, w.cost.n_classes, w.prob.n
+    cnt = got["cnt"].reshape(-1, X, NC, n)
+    assert cnt[4].sum() == 0 and cnt[5].sum() == 0
+    assert got["seg_count"].reshape(-1, NC)[4].sum() == 0
+    assert np.all(got["carbon"].reshape(-1, X)[4] == 0)
+    # other regions are untouched: region 1 equals the oracle run on the good offsets
+    want = oracle.closed_loop(w.prob, w.cost, 50, w.spec.seg_offsets, toks, fl)
+    lo, hi = T * X, 2 * T * X
+    np.testing.assert_array_equal(got["cnt"].reshape(-1, NC, n)[lo:hi], want["cnt"][lo:hi])
