@@ -108,6 +108,27 @@ def _bind(L):
                                   _i64p, _u16p, C.c_int64, _u8p, _dp, _u64p, _u8p, _dp, _dp, _u64p, _u64p, _dp, _dp,
                                   _dp, _dp]
     L.orc_closed_loop.restype = C.c_int
+    L.orc_pref_word.argtypes = [C.c_uint64, C.c_uint64]
+    L.orc_pref_word.restype = C.c_uint32
+    L.orc_pref_level.argtypes = [C.c_int, _dp, C.c_uint64, C.c_uint64]
+    L.orc_pref_level.restype = C.c_int
+    L.orc_normalized_preference.argtypes = [C.c_double]
+    L.orc_normalized_preference.restype = C.c_double
+    L.orc_head_to_head.argtypes = [C.c_int, C.c_int, _ip, _ip]
+    L.orc_head_to_head.restype = None
+    L.orc_preference.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                 C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, _i64p, _u8p, C.c_int,
+                                 C.c_int, _u64p]
+    L.orc_preference.restype = C.c_int
+    L.orc_request_outputs.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                      C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp, _dp,
+                                      _i64p, _u16p, C.c_int64, _u8p, C.c_int, C.c_int, C.c_int,
+                                      _u8p, _dp, _dp, _dp, _u8p]
+    L.orc_request_outputs.restype = C.c_int
+    L.orc_oracle_scheme.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_int,
+                                    C.c_double, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp, _dp,
+                                    _i64p, _u16p, C.c_int64, _u8p, _u64p, _u64p, _dp, _dp, _dp, _dp, _u64p, _u8p]
+    L.orc_oracle_scheme.restype = C.c_int
     return L
 
 
@@ -354,4 +375,92 @@ def closed_loop(prob, cost, window: int, seg_offsets, tokens, flags=None):
     if st != 0:
         raise ValueError("oracle closed_loop: invalid argument")
     out["threshold"] = out["threshold"][:, : n - 1]
+    return out
+
+
+# --------------------------------------------------------------------------
+# NEXT-4: latent preference, head-to-head preference, per-request outputs,
+# the Oracle scheme (readings L21-L23)
+
+def pref_word(seed: int, g: int) -> int:
+    return int(lib().orc_pref_word(C.c_uint64(int(seed)), C.c_uint64(int(g))))
+
+
+def pref_level(q, seed: int, g: int) -> int:
+    q = _f64(q)
+    return int(lib().orc_pref_level(len(q), _p(q, _dp), C.c_uint64(int(seed)), C.c_uint64(int(g))))
+
+
+def normalized_preference(w: float) -> float:
+    """w / (1 - w) for the scheme's head-to-head win fraction w."""
+    return float(lib().orc_normalized_preference(float(w)))
+
+
+def head_to_head(L: int, lstar: int):
+    win, loss = C.c_int(0), C.c_int(0)
+    lib().orc_head_to_head(int(L), int(lstar), C.byref(win), C.byref(loss))
+    return win.value, loss.value
+
+
+def _problem_args(prob):
+    return (prob.n, prob.R, int(prob.T), prob.X, _p(_f64(prob.k0), _dp), _p(_f64(prob.kmin), _dp),
+            _p(_f64(prob.kmax), _dp), _p(_f64(prob.xi), _dp), _p(_f64(prob.e), _dp), _p(_f64(prob.p), _dp),
+            _p(_f64(prob.q), _dp), int(prob.profile_per_interval), float(prob.k1), float(prob.pue))
+
+
+def preference(prob, cost, seg_offsets, flags=None, scheme: int = 0, grid_den: int = 0):
+    """Per cell [R*T*X][3]: hits (L = l*), wins, losses against Base (reading L22)."""
+    keep = [_f64(a) for a in (prob.k0, prob.kmin, prob.kmax, prob.xi, prob.e, prob.p, prob.q)]
+    off = np.ascontiguousarray(seg_offsets, dtype=np.int64)
+    fl = None if flags is None else np.ascontiguousarray(flags, dtype=np.uint8)
+    out = np.zeros((prob.R * prob.T * prob.X, 3), np.uint64)
+    st = lib().orc_preference(*_problem_args(prob), C.c_uint64(int(cost.seed)), int(cost.n_classes),
+                              _p(off, _i64p), _p(fl, _u8p), int(scheme), int(grid_den), _p(out, _u64p))
+    del keep
+    if st != 0:
+        raise ValueError("oracle preference: invalid argument")
+    return out
+
+
+def request_outputs(prob, cost, seg_offsets, tokens, flags=None, j: int = 0, scheme: int = 0, grid_den: int = 0):
+    """Per request of cell column j: level, carbon, Base carbon, ratio (Fig. eval2), l*."""
+    off = np.ascontiguousarray(seg_offsets, dtype=np.int64)
+    tokens = np.ascontiguousarray(tokens, dtype=np.uint16)
+    fl = None if flags is None else np.ascontiguousarray(flags, dtype=np.uint8)
+    N = int(off[-1])
+    out = dict(level=np.zeros(N, np.uint8), carbon=np.zeros(N), base=np.zeros(N), ratio=np.zeros(N),
+               pref=np.zeros(N, np.uint8))
+    ef, et, pf, pt = (_f64(a) for a in (cost.ef, cost.et, cost.pf, cost.pt))
+    st = lib().orc_request_outputs(*_problem_args(prob), C.c_uint64(int(cost.seed)), int(cost.n_classes),
+                                   _p(ef, _dp), _p(et, _dp), _p(pf, _dp), _p(pt, _dp), _p(off, _i64p),
+                                   _p(tokens, _u16p), tokens.shape[1], _p(fl, _u8p), int(scheme), int(grid_den),
+                                   int(j), _p(out["level"], _u8p), _p(out["carbon"], _dp), _p(out["base"], _dp),
+                                   _p(out["ratio"], _dp), _p(out["pref"], _u8p))
+    if st != 0:
+        raise ValueError("oracle request_outputs: invalid argument")
+    return out
+
+
+def oracle_scheme(prob, cost, seg_offsets, tokens, flags=None):
+    """The Oracle scheme (reading L23), per cell: cnt/tok [NC][n],
+    energy/time/carbon/quality sums, stats (hits, wins, losses), status."""
+    n, R, T, X, NC = prob.n, prob.R, int(prob.T), prob.X, cost.n_classes
+    off = np.ascontiguousarray(seg_offsets, dtype=np.int64)
+    tokens = np.ascontiguousarray(tokens, dtype=np.uint16)
+    fl = None if flags is None else np.ascontiguousarray(flags, dtype=np.uint8)
+    cells = R * T * X
+    out = dict(cnt=np.zeros((cells, NC, n), np.uint64), tok=np.zeros((cells, NC, n), np.uint64),
+               energy=np.zeros(cells), time=np.zeros(cells), carbon=np.zeros(cells), quality=np.zeros(cells),
+               stats=np.zeros((cells, 3), np.uint64), status=np.zeros(cells, np.uint8))
+    ef, et, pf, pt = (_f64(a) for a in (cost.ef, cost.et, cost.pf, cost.pt))
+    st = lib().orc_oracle_scheme(n, R, T, X, _p(_f64(prob.k0), _dp), _p(_f64(prob.kmin), _dp),
+                                 _p(_f64(prob.kmax), _dp), _p(_f64(prob.xi), _dp), _p(_f64(prob.q), _dp),
+                                 int(prob.profile_per_interval), float(prob.k1), float(prob.pue),
+                                 C.c_uint64(int(cost.seed)), NC, _p(ef, _dp), _p(et, _dp), _p(pf, _dp), _p(pt, _dp),
+                                 _p(off, _i64p), _p(tokens, _u16p), tokens.shape[1], _p(fl, _u8p),
+                                 _p(out["cnt"], _u64p), _p(out["tok"], _u64p), _p(out["energy"], _dp),
+                                 _p(out["time"], _dp), _p(out["carbon"], _dp), _p(out["quality"], _dp),
+                                 _p(out["stats"], _u64p), _p(out["status"], _u8p))
+    if st != 0:
+        raise ValueError("oracle oracle_scheme: invalid argument")
     return out

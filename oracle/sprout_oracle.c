@@ -874,3 +874,256 @@ int orc_closed_loop(int n, int R, int64_t T, int X,
     free(ring_c); free(ring_t);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: the latent preferred level, head-to-head preference
+ * against Base, per-request outputs, and the Oracle scheme.                 */
+
+/* Reading L21.  The evaluator "generates responses for each [sampled prompt]
+ * at all generation directive levels, and identifies the directive level that
+ * yields the best response for each request"; q holds the preference
+ * rates of those levels.  Synthetic ground truth: request g's latent
+ * best level l*(g) is the inverse-CDF level of q -- the a4/a6 rules with q in
+ * place of the mix x -- at the word of Philox stream 2: key (seed lo, seed
+ * hi), counter (g>>2 lo32, g>>2 hi32, 2, 0), word g & 3.                     */
+uint32_t orc_pref_word(uint64_t seed, uint64_t g)
+{
+    uint32_t key[2] = { (uint32_t)seed, (uint32_t)(seed >> 32) };
+    uint64_t blk = g >> 2;
+    uint32_t ctr[4] = { (uint32_t)blk, (uint32_t)(blk >> 32), 2u, 0u };
+    uint32_t out[4];
+    orc_philox4x32_10(ctr, key, out);
+    return out[g & 3u];
+}
+
+int orc_pref_level(int n, const double *q, uint64_t seed, uint64_t g)
+{
+    return orc_select_level(n, q, orc_pref_word(seed, g), 0);
+}
+
+/* "if the auto-evaluator shows a preference for Sprout's responses 48%
+ * of the time versus 52% for Base, Sprout's normalized generation preference
+ * score would be 92.3%": score = w / (1 - w).  No finite score at w = 1.     */
+double orc_normalized_preference(double w)
+{
+    return w >= 1.0 ? INFINITY : w / (1.0 - w);
+}
+
+/* Reading L22: the head-to-head of a scheme's response (level L) against
+ * Base's (L0) for a request whose latent best level is l*: L = 0 gives
+ * the identical response, a tie; otherwise the scheme wins iff l* = L, Base
+ * wins iff l* = 0, and a third best level is a tie.  Ties count half:
+ * w = (wins + ties/2) / m.                                                   */
+void orc_head_to_head(int L, int lstar, int *win, int *loss)
+{
+    *win = (L != 0 && lstar == L);
+    *loss = (L != 0 && lstar == 0);
+}
+
+/* Per-cell preference statistics of a scheme's run (levels by each cell's
+ * mix, a6): stats[cell][0..2] = hits (L = l*, the realised Eq. 3 left-hand
+ * side), wins, losses against Base.  Requests with an invalid class and
+ * invalid cells are skipped.  Arguments as orc_simulate_scheme (all R*T
+ * segments; request g = global index).                                      */
+int orc_preference(int n, int R, int64_t T, int X,
+                   const double *k0, const double *kmin, const double *kmax, const double *xi,
+                   const double *e, const double *p, const double *q, int profile_per_interval,
+                   double k1, double pue, uint64_t seed, int n_classes,
+                   const int64_t *seg_offsets, const uint8_t *flags, int scheme, int grid_den,
+                   uint64_t *stats)
+{
+    if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1) return 1;
+    if (n_classes < 1 || n_classes > ORC_MAX_CLASSES) return 1;
+    if (!scheme_args_ok(n, X, scheme, grid_den)) return 1;
+    orc_problem P = { n, R, X, profile_per_interval, n_classes, T, k0, kmin, kmax, xi, e, p, q, k1, pue,
+                      scheme, grid_den };
+    double xs[ORC_MAX_LEVELS];
+    for (int64_t s = 0; s < (int64_t)R * T; ++s) {
+        const double *qs = prof(&P, q, s);
+        for (int j = 0; j < X; ++j) {
+            double obj, qlb; int vid, ml; uint64_t Tl[ORC_MAX_LEVELS];
+            uint64_t *st = stats + ((size_t)s * X + j) * 3;
+            st[0] = st[1] = st[2] = 0;
+            if (solve_cell(&P, s, j, xs, &obj, &qlb, &vid, Tl, &ml) != 0) continue;
+            for (int64_t g = seg_offsets[s]; g < seg_offsets[s + 1]; ++g) {
+                int pinned = 0, cls = 0;
+                if (flags) { pinned = flags[g] & 1; cls = (flags[g] >> 1) & 3; }
+                if (cls >= n_classes) continue;
+                const int L = orc_select_level(n, xs, orc_draw_word(seed, (uint64_t)g), pinned);
+                const int ls = orc_pref_level(n, qs, seed, (uint64_t)g);
+                int win, loss;
+                orc_head_to_head(L, ls, &win, &loss);
+                st[0] += (uint64_t)(L == ls);
+                st[1] += (uint64_t)win;
+                st[2] += (uint64_t)loss;
+            }
+        }
+    }
+    return 0;
+}
+
+/* Per-request outputs of cell column j (one xi value) of a scheme's run:
+ * for every request g of segments [0, R*T): its level, its carbon (Eq. 1,
+ * P:50-54, at its segment's CI), the carbon it would have under Base (all
+ * at L0), their ratio -- the per-request carbon normalised to Base of
+ * Fig. eval2 -- and its latent best level.  Invalid class or cell:
+ * level 0xFF, carbon and ratio NaN.                                         */
+int orc_request_outputs(int n, int R, int64_t T, int X,
+                        const double *k0, const double *kmin, const double *kmax, const double *xi,
+                        const double *e, const double *p, const double *q, int profile_per_interval,
+                        double k1, double pue, uint64_t seed, int n_classes,
+                        const double *ef, const double *et, const double *pf, const double *pt,
+                        const int64_t *seg_offsets, const uint16_t *tokens, int64_t pitch,
+                        const uint8_t *flags, int scheme, int grid_den, int j,
+                        uint8_t *level, double *carbon, double *base, double *ratio, uint8_t *pref)
+{
+    if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1 || j < 0 || j >= X) return 1;
+    if (n_classes < 1 || n_classes > ORC_MAX_CLASSES) return 1;
+    if (!scheme_args_ok(n, X, scheme, grid_den)) return 1;
+    orc_problem P = { n, R, X, profile_per_interval, n_classes, T, k0, kmin, kmax, xi, e, p, q, k1, pue,
+                      scheme, grid_den };
+    double xs[ORC_MAX_LEVELS];
+    for (int64_t s = 0; s < (int64_t)R * T; ++s) {
+        double obj, qlb; int vid, ml; uint64_t Tl[ORC_MAX_LEVELS];
+        const int ok = solve_cell(&P, s, j, xs, &obj, &qlb, &vid, Tl, &ml) == 0;
+        const double kp = P.k0[s] * pue;
+        const double *qs = prof(&P, q, s);
+        for (int64_t g = seg_offsets[s]; g < seg_offsets[s + 1]; ++g) {
+            int pinned = 0, cls = 0;
+            if (flags) { pinned = flags[g] & 1; cls = (flags[g] >> 1) & 3; }
+            pref[g] = (uint8_t)orc_pref_level(n, qs, seed, (uint64_t)g);
+            if (!ok || cls >= n_classes) {
+                level[g] = 0xFF; carbon[g] = NAN; base[g] = NAN; ratio[g] = NAN;
+                continue;
+            }
+            const int L = orc_select_level(n, xs, orc_draw_word(seed, (uint64_t)g), pinned);
+            const double tl = (double)tokens[(size_t)L * pitch + g], t0 = (double)tokens[g];
+            const double el = ef[cls * 8 + L] + et[cls * 8 + L] * tl, pl = pf[cls * 8 + L] + pt[cls * 8 + L] * tl;
+            const double e0 = ef[cls * 8] + et[cls * 8] * t0, p0 = pf[cls * 8] + pt[cls * 8] * t0;
+            level[g] = (uint8_t)L;
+            carbon[g] = orc_request_carbon(kp, k1, el, pl);
+            base[g] = orc_request_carbon(kp, k1, e0, p0);
+            ratio[g] = carbon[g] / base[g];
+        }
+    }
+    return 0;
+}
+
+/* Reading L23 -- the Oracle scheme (it "assumes the inference carbon
+ * emission on every generation directive level is known ahead of time for
+ * all user prompts, and knows the exact generation quality feedback for
+ * future prompts").  Per cell (segment, xi): with every request's carbon at
+ * every level (Eq. 1) and its latent best level l*, choose each request's
+ * level to minimise the cell's carbon subject to the realised quality
+ * #{g : L(g) = l*(g)} >= k = ceil(fl(b * m)), b the cell's Eq. 3 floor
+ * and m its valid requests; opted-out requests stay at L0
+ * (P:240).  Any level other than a request's cheapest level m(g) (lowest
+ * index among equal carbon) or its l* is dominated, so the optimum serves
+ * every request at m(g) and moves the (k - free hits) requests with
+ * l* != m(g) of smallest extra carbon Delta = C_l* - C_m(g) (equal Delta:
+ * lower request index first) to l*: a unit-gain selection, exact by the
+ * exchange argument.  Too few candidates: all move, status 2.  Invalid cell
+ * inputs: status 1, totals 0.  Outputs per cell: cnt/tok [NC][n], fp64 sums
+ * of E, T, carbon and q[level] over the requests in index order, stats
+ * (hits, wins, losses as orc_preference) and status.                        */
+typedef struct { double d; int64_t g; } orc_cand;
+static int cand_cmp(const void *a, const void *b)
+{
+    const orc_cand *x = (const orc_cand *)a, *y = (const orc_cand *)b;
+    if (x->d < y->d) return -1;
+    if (x->d > y->d) return 1;
+    return (x->g > y->g) - (x->g < y->g);
+}
+
+int orc_oracle_scheme(int n, int R, int64_t T, int X,
+                      const double *k0, const double *kmin, const double *kmax, const double *xi,
+                      const double *q, int profile_per_interval, double k1, double pue,
+                      uint64_t seed, int n_classes, const double *ef, const double *et,
+                      const double *pf, const double *pt,
+                      const int64_t *seg_offsets, const uint16_t *tokens, int64_t pitch, const uint8_t *flags,
+                      uint64_t *cnt, uint64_t *tok, double *energy, double *time_s, double *carbon,
+                      double *quality, uint64_t *stats, uint8_t *status)
+{
+    if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1) return 1;
+    if (n_classes < 1 || n_classes > ORC_MAX_CLASSES) return 1;
+    const int NC = n_classes;
+    for (int64_t s = 0; s < (int64_t)R * T; ++s) {
+        const int64_t r = s / T, g0 = seg_offsets[s], m_all = seg_offsets[s + 1] - g0;
+        const double *qs = q + (profile_per_interval ? s : r) * n;
+        const double kp = k0[s] * pue;
+        /* per request: class, pinned, cheapest level, l*, the base choice */
+        int *cls = (int *)malloc(sizeof(int) * (size_t)(m_all > 0 ? m_all : 1));
+        int *lm = (int *)malloc(sizeof(int) * (size_t)(m_all > 0 ? m_all : 1));
+        int *ls = (int *)malloc(sizeof(int) * (size_t)(m_all > 0 ? m_all : 1));
+        int *ch = (int *)malloc(sizeof(int) * (size_t)(m_all > 0 ? m_all : 1));
+        orc_cand *cand = (orc_cand *)malloc(sizeof(orc_cand) * (size_t)(m_all > 0 ? m_all : 1));
+        int64_t m = 0, free_hits = 0, nc = 0;
+        for (int64_t i = 0; i < m_all; ++i) {
+            const int64_t g = g0 + i;
+            int pinned = 0, c = 0;
+            if (flags) { pinned = flags[g] & 1; c = (flags[g] >> 1) & 3; }
+            cls[i] = c;
+            if (c >= NC) continue;
+            ++m;
+            double C[ORC_MAX_LEVELS];
+            for (int L = 0; L < n; ++L) {
+                const double t = (double)tokens[(size_t)L * pitch + g];
+                C[L] = orc_request_carbon(kp, k1, ef[c * 8 + L] + et[c * 8 + L] * t, pf[c * 8 + L] + pt[c * 8 + L] * t);
+            }
+            int best = 0;
+            for (int L = 1; L < n; ++L) if (C[L] < C[best]) best = L;
+            lm[i] = best;
+            ls[i] = orc_pref_level(n, qs, seed, (uint64_t)g);
+            ch[i] = pinned ? 0 : best;
+            free_hits += (ch[i] == ls[i]);
+            if (!pinned && ls[i] != best) {
+                cand[nc].d = C[ls[i]] - C[best];
+                cand[nc].g = i;
+                ++nc;
+            }
+        }
+        qsort(cand, (size_t)nc, sizeof(orc_cand), cand_cmp);
+        uint8_t *moved = (uint8_t *)malloc((size_t)(m_all > 0 ? m_all : 1));
+        for (int j = 0; j < X; ++j) {
+            const int64_t cell = s * X + j;
+            uint64_t *cn = cnt + (size_t)cell * NC * n, *tk = tok + (size_t)cell * NC * n;
+            uint64_t *st = stats + (size_t)cell * 3;
+            memset(cn, 0, sizeof(uint64_t) * NC * n);
+            memset(tk, 0, sizeof(uint64_t) * NC * n);
+            st[0] = st[1] = st[2] = 0;
+            energy[cell] = 0.0; time_s[cell] = 0.0; carbon[cell] = 0.0; quality[cell] = 0.0;
+            double dummy_e[ORC_MAX_LEVELS], dummy_p[ORC_MAX_LEVELS];
+            for (int L = 0; L < n; ++L) { dummy_e[L] = 0.0; dummy_p[L] = 0.0; }
+            if (!cell_inputs_valid(n, k0[s], kmin[r], kmax[r], xi[j], dummy_e, dummy_p, qs)) {
+                status[cell] = 1;
+                continue;
+            }
+            const double b = orc_quality_lower_bound(k0[s], kmin[r], kmax[r], xi[j], qs[0]);
+            const double bm = ceil(b * (double)m);
+            int64_t need = (int64_t)bm - free_hits;
+            if (need < 0) need = 0;
+            status[cell] = need > nc ? 2 : 0;
+            if (need > nc) need = nc;
+            memset(moved, 0, (size_t)(m_all > 0 ? m_all : 1));
+            for (int64_t k = 0; k < need; ++k) moved[cand[k].g] = 1;
+            double E = 0.0, Tm = 0.0, Cb = 0.0, Q = 0.0;
+            for (int64_t i = 0; i < m_all; ++i) {
+                const int c = cls[i];
+                if (c >= NC) continue;
+                const int64_t g = g0 + i;
+                const int L = moved[i] ? ls[i] : ch[i];
+                const uint32_t t = tokens[(size_t)L * pitch + g];
+                const double el = ef[c * 8 + L] + et[c * 8 + L] * (double)t;
+                const double pl = pf[c * 8 + L] + pt[c * 8 + L] * (double)t;
+                E += el; Tm += pl; Cb += orc_request_carbon(kp, k1, el, pl); Q += qs[L];
+                cn[c * n + L] += 1; tk[c * n + L] += t;
+                int win, loss;
+                orc_head_to_head(L, ls[i], &win, &loss);
+                st[0] += (uint64_t)(L == ls[i]); st[1] += (uint64_t)win; st[2] += (uint64_t)loss;
+            }
+            energy[cell] = E; time_s[cell] = Tm; carbon[cell] = Cb; quality[cell] = Q;
+        }
+        free(moved); free(cls); free(lm); free(ls); free(ch); free(cand);
+    }
+    return 0;
+}
