@@ -377,6 +377,53 @@ sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int3
                                           const sprout_cell_totals *totals, double *profile_out,
                                           sprout_stream stream);
 
+/* ---------------------------------------------------------------------- */
+/* NEXT-4: per-request outputs, the latent best level and the
+ * head-to-head preference against Base, and the Oracle scheme.
+ *
+ * Reading L21 (latent best level): the evaluator "identifies the directive
+ * level that yields the best response for each request" and q holds
+ * the preference rates of those levels.  Synthetic ground truth:
+ * request g's latent best level l*(g) is the inverse-CDF level of its
+ * segment's q row (the rules a4/a6 with q in place of the mix) at the word
+ * of Philox4x32-10 stream 2: key (seed lo, seed hi), counter (g>>2 lo32,
+ * g>>2 hi32, 2, 0), word g & 3 (the selection draw is stream 0).
+ * Reading L22 (head-to-head vs Base): a request served at L = 0 ties
+ * (identical response); otherwise the scheme wins iff l* = L and Base wins
+ * iff l* = 0, a third best level ties.  w = (wins + ties/2) / requests and
+ * the normalized preference score is w / (1 - w)
+ * (sprout_normalized_preference; w = 0.48 -> 0.923). */
+
+/* Per-request outputs of cell column xi_index (one xi value) of a solved
+ * (solution) sweep -- the per-request carbon normalised to Base behind the
+ * CDF of Fig. eval2.  For every local request r of a valid segment:
+ * level_out[r] its level (a6; 0xFF for an invalid class or cell),
+ * carbon_out[r] its Eq. 1 carbon at its level and its segment's CI,
+ * base_out[r] its carbon at L0 (Base), ratio_out[r] = carbon / base
+ * (NaN when invalid), and pref_out[r] (may be NULL) its l*.  Same operation
+ * order as the accounting of sprout_simulate_trace per request (no FMA).
+ * All arrays device, [n_requests].  Errors: INVALID_ARGUMENT (as
+ * sprout_simulate_trace; xi_index outside [0, n_xi); NULL or misaligned
+ * outputs); CUDA. */
+sprout_status sprout_request_outputs(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                     const sprout_trace *trace, const sprout_cost_model *cost, int32_t xi_index,
+                                     uint8_t *level_out, double *carbon_out, double *base_out, double *ratio_out,
+                                     uint8_t *pref_out, sprout_stream stream);
+
+/* Head-to-head statistics per cell of a solved sweep: stats[cell][0..2] =
+ * hits (requests at their latent best level: the realised Eq. 3 left-hand
+ * side), wins and losses against Base (reading L22); u64, device,
+ * [n_segments * n_xi][3].  Requests with an invalid class, invalid cells and
+ * invalid segments count nothing.  n_xi * 12 bytes <= 200 KiB.  Errors as
+ * sprout_request_outputs. */
+sprout_status sprout_preference_stats(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                      const sprout_trace *trace, const sprout_cost_model *cost, uint64_t *stats,
+                                      sprout_stream stream);
+
+/* P:377's normalized preference score w / (1 - w) of a head-to-head win
+ * fraction w in [0, 1] (+inf at w = 1; NaN for w < 0 or NaN).  Host. */
+double sprout_normalized_preference(double w);
+
 /* Number of kernel launches (not memsets) the last successful call of each
  * entry point on this thread enqueued -- for launch accounting in benches. */
 int32_t sprout_last_launch_count(void);

@@ -311,6 +311,68 @@ sprout_status sprout_simulate_trace_bounded(const sprout_lp_problem *problem, co
     return st;
 }
 
+static sprout_status n4_args(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                             const sprout_trace *trace, const sprout_cost_model *cost, N4Args &a) {
+    sprout_status st = validate_problem(problem);
+    if (st == SPROUT_OK) st = validate_solution(problem, solution);
+    if (st == SPROUT_OK) st = validate_trace(problem, trace);
+    if (st == SPROUT_OK) st = validate_cost(cost);
+    if (st != SPROUT_OK) return st;
+    a = N4Args{};
+    a.n = problem->n_levels; a.X = problem->n_xi; a.NC = cost->n_classes;
+    a.T = problem->n_intervals; a.first_segment = problem->first_segment; a.n_segments = problem->n_segments;
+    a.profile_per_interval = problem->profile_per_interval;
+    a.k0 = problem->k0; a.q = problem->q; a.k1 = problem->k1; a.pue = problem->pue;
+    a.threshold = solution->threshold; a.max_level = solution->max_level; a.cell_status = solution->cell_status;
+    a.n_requests = trace->n_requests; a.first_request = trace->first_request; a.seg_offsets = trace->seg_offsets;
+    a.tokens = trace->tokens; a.pitch = trace->plane_pitch; a.flags = trace->flags; a.seed = cost->seed;
+    std::memcpy(a.cost.ef, cost->ef, sizeof(cost->ef));
+    std::memcpy(a.cost.et, cost->et, sizeof(cost->et));
+    std::memcpy(a.cost.pf, cost->pf, sizeof(cost->pf));
+    std::memcpy(a.cost.pt, cost->pt, sizeof(cost->pt));
+    return SPROUT_OK;
+}
+
+sprout_status sprout_request_outputs(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                     const sprout_trace *trace, const sprout_cost_model *cost, int32_t xi_index,
+                                     uint8_t *level_out, double *carbon_out, double *base_out, double *ratio_out,
+                                     uint8_t *pref_out, sprout_stream stream) {
+    N4Args a;
+    sprout_status st = n4_args(problem, solution, trace, cost, a);
+    if (st != SPROUT_OK) return st;
+    if (xi_index < 0 || xi_index >= problem->n_xi) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (trace->n_requests > 0 && (!level_out || !carbon_out || !base_out || !ratio_out || !aligned(carbon_out, 8) ||
+                                  !aligned(base_out, 8) || !aligned(ratio_out, 8)))
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    a.column = xi_index;
+    a.level_out = level_out; a.carbon_out = carbon_out; a.base_out = base_out; a.ratio_out = ratio_out;
+    a.pref_out = pref_out;
+    int launches = 0;
+    st = cuda_status(launch_request_outputs(a, reinterpret_cast<cudaStream_t>(stream), &launches));
+    if (st == SPROUT_OK) g_last_launches = launches;
+    return st;
+}
+
+sprout_status sprout_preference_stats(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                      const sprout_trace *trace, const sprout_cost_model *cost, uint64_t *stats,
+                                      sprout_stream stream) {
+    N4Args a;
+    sprout_status st = n4_args(problem, solution, trace, cost, a);
+    if (st != SPROUT_OK) return st;
+    if (problem->n_segments > 0 && (!stats || !aligned(stats, 8))) return SPROUT_ERR_INVALID_ARGUMENT;
+    if ((size_t)problem->n_xi * 12 > 200 * 1024) return SPROUT_ERR_INVALID_ARGUMENT;
+    a.stats = stats;
+    int launches = 0;
+    st = cuda_status(launch_pref_stats(a, reinterpret_cast<cudaStream_t>(stream), &launches));
+    if (st == SPROUT_OK) g_last_launches = launches;
+    return st;
+}
+
+double sprout_normalized_preference(double w) {
+    if (!(w >= 0.0)) return std::nan("");
+    return w >= 1.0 ? HUGE_VAL : w / (1.0 - w);
+}
+
 int32_t sprout_group_stat_count(int32_t n_levels) { return 11 + 2 * n_levels; }
 
 size_t sprout_reduce_workspace_bytes(const sprout_lp_problem *problem) {

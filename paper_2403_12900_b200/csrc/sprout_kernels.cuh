@@ -78,6 +78,29 @@ struct ClosedArgs {             // closed-loop profiles (closed_loop.cu)
     uint32_t *trace_status;
 };
 
+struct N4Args {                 // NEXT-4 kernels (next4.cu)
+    int n, X, NC;
+    int64_t T, first_segment, n_segments;
+    int profile_per_interval;
+    const double *k0, *q;
+    double k1, pue;
+    const uint32_t *threshold;
+    const uint8_t *max_level, *cell_status;
+    int64_t n_requests;
+    uint64_t first_request;
+    const int64_t *seg_offsets;
+    const uint16_t *tokens;
+    int64_t pitch;
+    const uint8_t *flags;
+    uint64_t seed;
+    uint32_t rk0[10], rk1[10];
+    CostConst cost;
+    int column;                // request outputs: the xi column
+    uint8_t *level_out, *pref_out;
+    double *carbon_out, *base_out, *ratio_out;
+    uint64_t *stats;           // [cells][3] hits, wins, losses
+};
+
 struct EvalArgs {               // evaluator trigger sweep (evaluator.cu)
     int R, B, H, F;
     int grace_samples;         // least s >= 0 with s * dt >= grace (fp64, as the definition reads)
@@ -190,6 +213,8 @@ cudaError_t launch_reduce(ReduceArgs &a, void *ws, cudaStream_t stream, int *lau
 cudaError_t launch_generate(const GenArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_evaluator(const EvalArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_closed_loop(ClosedArgs &a, cudaStream_t stream, int *launches);
+cudaError_t launch_request_outputs(N4Args &a, cudaStream_t stream, int *launches);
+cudaError_t launch_pref_stats(N4Args &a, cudaStream_t stream, int *launches);
 cudaError_t launch_select_static(const SelectArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_check_cells(const uint8_t *status, int64_t n_cells, uint32_t *out, cudaStream_t stream, int *launches);
 

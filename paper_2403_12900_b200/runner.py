@@ -109,6 +109,22 @@ class Sweep:
         S.simulate_closed_loop(self.dp, window, self.trace, self.cost, self.sol, self.totals, prof, stream)
         return prof
 
+    def request_outputs(self, xi_index: int, stream=None) -> dict:
+        """NEXT-4: per-request level, carbon, Base carbon, ratio and latent best level of one xi column."""
+        N, dev = self.trace.n_requests, self.device
+        out = dict(level=torch.empty(N, dtype=torch.uint8, device=dev), carbon=torch.empty(N, dtype=torch.float64, device=dev),
+                   base=torch.empty(N, dtype=torch.float64, device=dev), ratio=torch.empty(N, dtype=torch.float64, device=dev),
+                   pref=torch.empty(N, dtype=torch.uint8, device=dev))
+        S.request_outputs(self.dp, self.sol, self.trace, self.cost, xi_index, out["level"], out["carbon"],
+                          out["base"], out["ratio"], out["pref"], stream)
+        return out
+
+    def preference_stats(self, stream=None) -> torch.Tensor:
+        """NEXT-4: per cell (hits, wins, losses) against Base."""
+        st = torch.zeros((self.dp.cells, 3), dtype=torch.int64, device=self.device)
+        S.preference_stats(self.dp, self.sol, self.trace, self.cost, st, stream)
+        return st
+
     def reduce(self, stream=None):
         S.reduce_totals(self.dp, self.sol, self.totals, self.n_classes, self.group, self.rws, stream)
 

@@ -398,3 +398,33 @@ def status_string(status: int) -> str:
 def workspace(nbytes: int, device) -> torch.Tensor:
     """A 256-byte aligned device byte buffer (torch's allocator aligns to 512)."""
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+# NEXT-4: per-request outputs, head-to-head preference statistics (readings L21, L22)
+_lib.sprout_request_outputs.argtypes = [_P(LpProblem), _P(LpSolution), _P(Trace), _P(CostModel), C.c_int32,
+                                        _vp, _vp, _vp, _vp, _vp, _vp]
+_lib.sprout_preference_stats.argtypes = [_P(LpProblem), _P(LpSolution), _P(Trace), _P(CostModel), _vp, _vp]
+_lib.sprout_normalized_preference.argtypes = [C.c_double]
+_lib.sprout_normalized_preference.restype = C.c_double
+
+
+def request_outputs(prob: DeviceProblem, sol: Solution, trace: DeviceTrace, cost: CostModel, xi_index: int,
+                    level_out: torch.Tensor, carbon_out: torch.Tensor, base_out: torch.Tensor,
+                    ratio_out: torch.Tensor, pref_out: Optional[torch.Tensor] = None, stream=None) -> None:
+    p, s, t = prob.c(), sol.c(), trace.c()
+    _check("sprout_request_outputs",
+           _lib.sprout_request_outputs(C.byref(p), C.byref(s), C.byref(t), C.byref(cost), int(xi_index),
+                                       _ptr(level_out), _ptr(carbon_out), _ptr(base_out), _ptr(ratio_out),
+                                       _ptr(pref_out), _stream(stream)))
+
+
+def preference_stats(prob: DeviceProblem, sol: Solution, trace: DeviceTrace, cost: CostModel, stats: torch.Tensor,
+                     stream=None) -> None:
+    p, s, t = prob.c(), sol.c(), trace.c()
+    _check("sprout_preference_stats",
+           _lib.sprout_preference_stats(C.byref(p), C.byref(s), C.byref(t), C.byref(cost), _ptr(stats),
+                                        _stream(stream)))
+
+
+def normalized_preference(w: float) -> float:
+    return float(_lib.sprout_normalized_preference(float(w)))

@@ -1,0 +1,57 @@
+"""GPU parity of NEXT-4 through the C ABI vs the oracle (readings L21-L23):
+per-request levels, latent best levels bit-exact and carbon / Base carbon /
+ratio bit-exact (same operation order, no FMA); per-cell head-to-head
+statistics bit-exact."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2403_12900_b200 import sprout as S
+    from paper_2403_12900_b200.runner import Sweep
+
+DEV = "cuda:0"
+
+
+def _sweep(name, **kw):
+    w = synth.make_workload(name, **kw)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, fl = synth.host_trace(w.spec, sh)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=fl)
+    sw.solve()
+    return w, sh, toks, fl, sw
+
+
+@pytest.mark.parametrize("name,kw,j", [("C1", {}, 0), ("C2", dict(n_requests=40_000, n_intervals=48), 2),
+                                       ("C3", dict(n_requests=30_000, n_intervals=96), 0),
+                                       ("C4", dict(n_requests=200_000, n_intervals=24), 37),
+                                       ("C5", dict(n_requests=40_000, n_intervals=24, n_regions=4), 0)])
+def test_request_outputs_bit_exact(name, kw, j):
+    w, sh, toks, fl, sw = _sweep(name, **kw)
+    got = {k: v.cpu().numpy() for k, v in sw.request_outputs(j).items()}
+    want = oracle.request_outputs(w.prob, w.cost, w.spec.seg_offsets, toks, fl, j=j)
+    np.testing.assert_array_equal(got["level"], want["level"])
+    np.testing.assert_array_equal(got["pref"], want["pref"])
+    for k in ("carbon", "base", "ratio"):
+        np.testing.assert_array_equal(got[k].view(np.uint64), want[k].view(np.uint64), err_msg=k)
+
+
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C2", dict(n_requests=40_000, n_intervals=48)),
+                                     ("C3", dict(n_requests=30_000, n_intervals=96)),
+                                     ("C4", dict(n_requests=150_000, n_intervals=12))])
+def test_preference_stats_bit_exact(name, kw):
+    w, sh, toks, fl, sw = _sweep(name, **kw)
+    got = sw.preference_stats().cpu().numpy().view(np.uint64)
+    want = oracle.preference(w.prob, w.cost, w.spec.seg_offsets, fl)
+    np.testing.assert_array_equal(got, want)
+
+
+def test_normalized_preference_host():
+    assert S.normalized_preference(0.48) == pytest.approx(0.923, abs=1e-3)
+    assert S.normalized_preference(0.5) == 1.0
+    assert S.normalized_preference(1.0) == float("inf")
