@@ -124,7 +124,8 @@ EXPORTS = ["sprout_solve_directives", "sprout_workspace_bytes", "sprout_simulate
            "sprout_sweep_workspace_bytes", "sprout_sweep_host", "sprout_generate_trace",
            "sprout_last_launch_count", "sprout_status_string", "sprout_solve_scheme", "sprout_static_grid_size",
            "sprout_select_static", "sprout_simulate_trace_bounded", "sprout_evaluator_sweep",
-           "sprout_simulate_closed_loop"]
+           "sprout_simulate_closed_loop", "sprout_request_outputs", "sprout_preference_stats",
+           "sprout_normalized_preference"]
 
 # competing schemes, include/sprout.h SPROUT_SCHEME_*
 SCHEME_SPROUT, SCHEME_CO2_OPT, SCHEME_STATIC_GRID = 0, 1, 2
