@@ -65,6 +65,7 @@ typedef enum {
 #define SPROUT_TRACE_BAD_CLASS   0x1u   /* a request's class (flags bits 1-2) >= n_classes: request skipped */
 #define SPROUT_TRACE_BAD_OFFSETS 0x2u   /* seg_offsets not non-decreasing within [0, n_requests]: segment skipped */
 #define SPROUT_TRACE_SLOW_PATH   0x100u /* informational: a segment needed the generic (slow) kernel path */
+#define SPROUT_TRACE_TOO_LONG    0x4u   /* Oracle scheme: a segment longer than max_segment_requests: skipped */
 
 /* ---------------------------------------------------------------------- */
 /* The directive LP over a (region x interval x xi) grid, Eqs. 2-7.        */
@@ -419,6 +420,31 @@ sprout_status sprout_request_outputs(const sprout_lp_problem *problem, const spr
 sprout_status sprout_preference_stats(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
                                       const sprout_trace *trace, const sprout_cost_model *cost, uint64_t *stats,
                                       sprout_stream stream);
+
+/* The Oracle scheme ("the inference carbon emission on every
+ * generation directive level is known ahead of time for all user prompts,
+ * and [it] knows the exact generation quality feedback for future prompts";
+ * reading L23).  Per cell (segment, xi): with every request's Eq. 1 carbon at
+ * every level and its latent best level l*, each request's level minimises
+ * the cell's carbon subject to the realised quality #{L(g) = l*(g)} >=
+ * ceil(fl(b * m)), b the cell's Eq. 3 floor and m its valid requests;
+ * opted-out requests stay at L0.  The optimum serves every request
+ * at its cheapest level (lowest index among ties) and moves the requests
+ * with l* != cheapest of smallest extra carbon (ties: lower request index)
+ * to l* until the floor is met.  Writes every field of `totals` (cells and
+ * segments, as sprout_simulate_trace; E/T/C/Q in its closed form from the
+ * integer statistics), stats [cells][3] = (hits, wins, losses) as
+ * sprout_preference_stats, and cell_status [cells] (0 ok; 1 invalid cell
+ * input; 2 the floor cannot be met even with every candidate moved -- all
+ * moved).  Segments longer than max_segment_requests are skipped with
+ * SPROUT_TRACE_TOO_LONG (their outputs zero); workspace >=
+ * sprout_oracle_scheme_workspace_bytes (256-byte aligned; 32 bytes per
+ * request of the longest segment per SM).  Errors: INVALID_ARGUMENT; CUDA. */
+size_t sprout_oracle_scheme_workspace_bytes(const sprout_lp_problem *problem, int64_t max_segment_requests);
+sprout_status sprout_simulate_oracle_scheme(const sprout_lp_problem *problem, const sprout_trace *trace,
+                                            const sprout_cost_model *cost, int64_t max_segment_requests,
+                                            const sprout_cell_totals *totals, uint64_t *stats, uint8_t *cell_status,
+                                            void *workspace, size_t workspace_bytes, sprout_stream stream);
 
 /* P:377's normalized preference score w / (1 - w) of a head-to-head win
  * fraction w in [0, 1] (+inf at w = 1; NaN for w < 0 or NaN).  Host. */

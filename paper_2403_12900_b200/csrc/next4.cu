@@ -233,3 +233,409 @@ cudaError_t launch_pref_stats(N4Args &a, cudaStream_t stream, int *launches) {
 }
 
 }  // namespace sprout
+
+namespace sprout {
+
+// ---- the Oracle scheme (reading L23) ----
+// One CTA per segment (persistent, a queue of segments).  Pass 1 over the
+// segment: every request's carbon at every level (Eq. 1), its cheapest level
+// m (lowest index among ties), its latent best level l*, the base choice
+// (opted-out: L0, else m) and its statistics; the candidates (not opted out,
+// l* != m) are compacted in request order with key = the bits of
+// Delta = C_l* - C_m (a non-negative double: bit order = value order) and
+// their move (class, m, l*, tokens at m and l*).  A stable LSD radix sort of
+// the keys (8 passes of 8 bits, passes with one digit skipped) orders them
+// by (Delta, request index).  Then every xi cell takes the first
+// need = ceil(b m) - base hits of them: chunk sums of the moves, a block
+// scan, and per cell the partial chunk.  Integer statistics are exact; fp64
+// totals follow from them in trace_sim.cu's closed form.
+constexpr int kOrThreads = 512;
+constexpr int kOrWarps = kOrThreads / 32;
+
+// per CTA: keys x2 (8 B), indices x2 (4 B), moves (8 B) per request of a segment, then the
+// chunk sums of the moves ([kOrThreads][<= 2*4*8 + 3] signed 64-bit)
+constexpr int kOrMaxMv = 2 * kMaxClasses * kMaxLevels + 3;
+__host__ __device__ inline size_t or_cta_bytes(int64_t cap) {
+    return (size_t)32 * (size_t)(cap > 0 ? cap : 1) + (size_t)kOrThreads * kOrMaxMv * 8;
+}
+
+// the queue ticket (256 B), then one scratch region per CTA of the persistent grid (one CTA per SM)
+size_t oracle_scheme_workspace_bytes(int64_t cap) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return 256 + (size_t)sms * or_cta_bytes(cap);
+}
+
+struct OrSmem {
+    uint32_t hist[kOrWarps][256];
+    uint32_t dtot[256];
+    int64_t seg;
+    int skip;
+};
+
+template <int N, int NCM>
+__global__ void __launch_bounds__(kOrThreads) oracle_scheme_kernel(const __grid_constant__ N4Args a) {
+    __shared__ OrSmem sm;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t cap = a.cap;
+    uint8_t *scr = a.scratch + (size_t)blockIdx.x * or_cta_bytes(cap);
+    unsigned long long *keyA = reinterpret_cast<unsigned long long *>(scr);
+    unsigned long long *keyB = keyA + cap;
+    uint32_t *idxA = reinterpret_cast<uint32_t *>(keyB + cap);
+    uint32_t *idxB = idxA + cap;
+    unsigned long long *move = reinterpret_cast<unsigned long long *>(idxB + cap);   // by local request index
+    const int NC = a.NC;
+    uint32_t err = 0u;
+    // layout of the per-segment sums (u64): [0, NCM*N) base cnt, [NCM*N, 2NCM*N) base tok,
+    // then hits, wins, losses, valid requests, candidates; segment: per class count, pinned, tok[N]
+    constexpr int B_CNT = 0, B_TOK = NCM * N, B_HIT = 2 * NCM * N, B_WIN = B_HIT + 1, B_LOSS = B_HIT + 2,
+                  B_M = B_HIT + 3, B_NC = B_HIT + 4, S_BASE = B_HIT + 5;   // + NCM * (N + 2)
+    constexpr int NSUM = S_BASE + NCM * (N + 2);
+    __shared__ unsigned long long tot[NSUM];
+    __shared__ unsigned long long red[kOrWarps][NSUM];
+    for (;;) {
+        if (tid == 0) sm.seg = (int64_t)atomicAdd(a.queue, 1u);
+        __syncthreads();
+        const int64_t sl = sm.seg;
+        if (sl >= a.n_segments) break;
+        const int64_t s = a.first_segment + sl, r = s / a.T;
+        const int64_t s0 = a.seg_offsets[sl], s1 = a.seg_offsets[sl + 1];
+        const bool good = s0 >= 0 && s0 <= s1 && s1 <= a.n_requests;
+        const bool fits = s1 - s0 <= cap;
+        if (tid == 0 && !good) err |= SPROUT_TRACE_BAD_OFFSETS;
+        if (tid == 0 && good && !fits) err |= SPROUT_TRACE_TOO_LONG;
+        const int64_t m_all = (good && fits) ? s1 - s0 : 0;
+        const double kp = __dmul_rn(a.k0[s], a.pue);
+        const double *qr = q_row(a, s);
+        uint32_t Tq[N > 1 ? N - 1 : 1];
+        int mlq;
+        vec_thresholds<N>(qr, Tq, mlq);
+        // ---- pass 1: tiles of kOrThreads * 4 requests (each thread an aligned quad) ----
+        uint32_t bc[NCM][N], bt[NCM][N], sc[NCM][N + 2];
+        uint32_t hit = 0u, win = 0u, loss = 0u, mv = 0u;
+#pragma unroll
+        for (int c = 0; c < NCM; ++c) {
+#pragma unroll
+            for (int L = 0; L < N; ++L) { bc[c][L] = 0u; bt[c][L] = 0u; }
+#pragma unroll
+            for (int f = 0; f < N + 2; ++f) sc[c][f] = 0u;
+        }
+        uint32_t ncand = 0u;   // candidates so far (block-uniform, running)
+        for (int64_t t0 = s0 & ~(int64_t)3; t0 < s0 + m_all; t0 += 4 * kOrThreads) {
+            const int64_t q0 = t0 + 4 * (int64_t)tid;
+            const uint64_t blk = (a.first_request + (uint64_t)q0) >> 2;
+            const bool anyq = q0 + 4 > s0 && q0 < s0 + m_all;
+            Philox4 dp;
+            if (anyq) dp = n4_words(a, blk, 2u);
+            unsigned long long key[4], mvk[4];
+            uint32_t isc = 0u;   // bit k: request k is a candidate
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int64_t rq = q0 + k;
+                key[k] = 0ull; mvk[k] = 0ull;
+                if (!(anyq && rq >= s0 && rq < s0 + m_all)) continue;
+                const uint32_t fb = a.flags ? a.flags[rq] : 0u;
+                const int c = (int)((fb >> 1) & 3u);
+                if (c >= NC) { err |= SPROUT_TRACE_BAD_CLASS; continue; }
+                const bool pinned = fb & 1u;
+                uint32_t tk[N];
+                double C[N];
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    tk[L] = a.tokens[(size_t)L * a.pitch + rq];
+                    C[L] = n4_carbon(a, kp, c, L, tk[L]);
+                }
+                int mbest = 0;
+#pragma unroll
+                for (int L = 1; L < N; ++L) mbest = C[L] < C[mbest] ? L : mbest;
+                int ls = n4_level<N>(dp.v[k], Tq, mlq, false);
+                const int ch = pinned ? 0 : mbest;
+                double cm = C[0], cl = C[0];
+                uint32_t tm = tk[0], tl = tk[0];
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    if (L == mbest) { cm = C[L]; tm = tk[L]; }
+                    if (L == ls) { cl = C[L]; tl = tk[L]; }
+                }
+#pragma unroll
+                for (int cc = 0; cc < NCM; ++cc) {
+                    if (cc != c) continue;
+                    sc[cc][0] += 1u;
+                    sc[cc][1] += pinned ? 1u : 0u;
+#pragma unroll
+                    for (int L = 0; L < N; ++L) {
+                        sc[cc][2 + L] += tk[L];
+                        if (L == ch) { bc[cc][L] += 1u; bt[cc][L] += tk[L]; }
+                    }
+                }
+                hit += ch == ls ? 1u : 0u;
+                win += (ch != 0 && ls == ch) ? 1u : 0u;
+                loss += (ch != 0 && ls == 0) ? 1u : 0u;
+                mv += 1u;
+                if (!pinned && ls != mbest) {
+                    isc |= 1u << k;
+                    key[k] = (unsigned long long)__double_as_longlong(__dsub_rn(cl, cm));
+                    mvk[k] = (unsigned long long)c | ((unsigned long long)mbest << 2) | ((unsigned long long)ls << 5) |
+                             ((unsigned long long)tm << 8) | ((unsigned long long)tl << 24);
+                }
+            }
+            // compaction in request order: block-wide exclusive scan of the candidate counts
+            const uint32_t cnt4 = __popc(isc);
+            uint32_t x = cnt4;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+                if (lane >= d) x += y;
+            }
+            if (lane == 31) sm.hist[0][warp] = x;
+            __syncthreads();
+            uint32_t base = ncand, total = 0u;
+            for (int w2 = 0; w2 < kOrWarps; ++w2) {
+                const uint32_t v = sm.hist[0][w2];
+                base += w2 < warp ? v : 0u;
+                total += v;
+            }
+            base += x - cnt4;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!((isc >> k) & 1u)) continue;
+                keyA[base] = key[k];
+                idxA[base] = (uint32_t)(q0 + k - s0);
+                move[q0 + k - s0] = mvk[k];
+                ++base;
+            }
+            ncand += total;
+            __syncthreads();   // sm.hist reused
+        }
+        // ---- block sums of pass 1 ----
+        {
+            int v = 0;
+            auto put = [&](uint32_t x) {
+                const uint32_t sx = __reduce_add_sync(0xFFFFFFFFu, x);
+                if (lane == 0) red[warp][v] = sx;
+                ++v;
+            };
+#pragma unroll
+            for (int c = 0; c < NCM; ++c)
+#pragma unroll
+                for (int L = 0; L < N; ++L) put(bc[c][L]);
+#pragma unroll
+            for (int c = 0; c < NCM; ++c)
+#pragma unroll
+                for (int L = 0; L < N; ++L) put(bt[c][L]);
+            put(hit); put(win); put(loss); put(mv); put(0u);
+#pragma unroll
+            for (int c = 0; c < NCM; ++c)
+#pragma unroll
+                for (int f = 0; f < N + 2; ++f) put(sc[c][f]);
+        }
+        __syncthreads();
+        if (tid < NSUM) {
+            unsigned long long t = 0ull;
+            for (int w2 = 0; w2 < kOrWarps; ++w2) t += red[w2][tid];
+            tot[tid] = tid == B_NC ? (unsigned long long)ncand : t;
+        }
+        __syncthreads();
+        const int64_t nc = (int64_t)ncand;
+        // ---- stable LSD radix sort of (key, index), 8 bits per pass ----
+        unsigned long long *ks = keyA, *kd = keyB;
+        uint32_t *is = idxA, *id = idxB;
+        const int64_t per = (nc + kOrWarps - 1) / kOrWarps;   // warp w: [w*per, (w+1)*per)
+        const int64_t lo = min(nc, (int64_t)warp * per), hi = min(nc, lo + per);
+        for (int pass = 0; pass < 8; ++pass) {
+            const int sh = 8 * pass;
+            for (int i = lane; i < 256; i += 32) sm.hist[warp][i] = 0u;
+            __syncwarp();
+            for (int64_t i = lo + lane; i < hi; i += 32) atomicAdd(&sm.hist[warp][(ks[i] >> sh) & 0xFFu], 1u);
+            __syncthreads();
+            // skip the pass if one digit holds every key (thread d: digit d's total)
+            if (tid == 0) sm.skip = 0;
+            if (tid < 256) {
+                uint32_t t = 0u;
+                for (int w2 = 0; w2 < kOrWarps; ++w2) t += sm.hist[w2][tid];
+                sm.dtot[tid] = t;
+            }
+            __syncthreads();
+            if (tid < 256 && (int64_t)sm.dtot[tid] == nc) sm.skip = 1;
+            __syncthreads();
+            if (sm.skip) continue;
+            // exclusive offsets in (digit, warp) order: thread d over its digit's warps, after the
+            // digits before it
+            if (tid < 256) {
+                uint32_t before = 0u;
+                for (int d = 0; d < tid; ++d) before += sm.dtot[d];
+                for (int w2 = 0; w2 < kOrWarps; ++w2) {
+                    const uint32_t v = sm.hist[w2][tid];
+                    sm.hist[w2][tid] = before;
+                    before += v;
+                }
+            }
+            __syncthreads();
+            // scatter, each warp its range in order: rank among equal digits by match_any
+            for (int64_t i0 = lo; i0 < hi; i0 += 32) {
+                const int64_t i = i0 + lane;
+                const bool in = i < hi;
+                const unsigned long long kv = in ? ks[i] : 0ull;
+                const uint32_t dg = in ? (uint32_t)((kv >> sh) & 0xFFu) : 256u + (uint32_t)lane;
+                const uint32_t peers = __match_any_sync(0xFFFFFFFFu, dg);
+                if (in) {
+                    const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
+                    const uint32_t pos = sm.hist[warp][dg] + rank;
+                    kd[pos] = kv;
+                    id[pos] = is[i];
+                }
+                __syncwarp();
+                if (in && (__ffs(peers) - 1) == lane) sm.hist[warp][dg] += __popc(peers);
+                __syncwarp();
+            }
+            __syncthreads();
+            unsigned long long *tk2 = ks; ks = kd; kd = tk2;
+            uint32_t *ti = is; is = id; id = ti;
+        }
+        // ---- chunk sums of the moves over the sorted candidates ----
+        // per move: cnt[c][m] -1, cnt[c][l*] +1, tok[c][m] -tok_m, tok[c][l*] +tok_l*, hits +1,
+        // wins +[l* != 0], losses -[m != 0 and l* == 0]
+        const int64_t chunk = (nc + kOrThreads - 1) / kOrThreads;
+        const int64_t c_lo = min(nc, (int64_t)tid * chunk), c_hi = min(nc, c_lo + chunk);
+        constexpr int MV = 2 * NCM * N + 3;   // [cnt c,L][tok c,L] hits wins losses (signed)
+        auto apply = [&](unsigned long long mvv, long long (&acc)[MV]) {
+            const int c = (int)(mvv & 3u), mf = (int)((mvv >> 2) & 7u), lt = (int)((mvv >> 5) & 7u);
+            const long long tm = (long long)((mvv >> 8) & 0xFFFFu), tl = (long long)((mvv >> 24) & 0xFFFFu);
+#pragma unroll
+            for (int cc = 0; cc < NCM; ++cc)
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    if (cc != c) continue;
+                    if (L == mf) { acc[cc * N + L] -= 1; acc[NCM * N + cc * N + L] -= tm; }
+                    if (L == lt) { acc[cc * N + L] += 1; acc[NCM * N + cc * N + L] += tl; }
+                }
+            acc[2 * NCM * N] += 1;
+            acc[2 * NCM * N + 1] += lt != 0 ? 1 : 0;
+            acc[2 * NCM * N + 2] -= (mf != 0 && lt == 0) ? 1 : 0;
+        };
+        long long acc[MV];
+#pragma unroll
+        for (int v = 0; v < MV; ++v) acc[v] = 0;
+        for (int64_t i = c_lo; i < c_hi; ++i) apply(move[is[i]], acc);
+        // block exclusive scan of the chunk sums ([kOrThreads][MV] signed, after the moves)
+        long long *csum = reinterpret_cast<long long *>(move + cap);
+        if (nc > 0) {
+#pragma unroll
+            for (int v = 0; v < MV; ++v) csum[(size_t)tid * MV + v] = acc[v];
+        }
+        __syncthreads();
+        if (tid < MV && nc > 0) {
+            long long run = 0;
+            for (int t2 = 0; t2 < kOrThreads; ++t2) {
+                const long long v = csum[(size_t)t2 * MV + tid];
+                csum[(size_t)t2 * MV + tid] = run;
+                run += v;
+            }
+        }
+        __syncthreads();
+        // ---- every xi cell of the segment ----
+        const double kmin_r = a.kmin[r], kmax_r = a.kmax[r], k0_s = a.k0[s];
+        const unsigned long long mreq = tot[B_M], hit0 = tot[B_HIT];
+        for (int j = tid; j < a.X; j += kOrThreads) {
+            const int64_t cell = sl * a.X + j;
+            const double xi = a.xi[j];
+            bool ok = (xi >= 0.0 && xi <= 1.0) && finite_nonneg(k0_s) && finite_nonneg(kmin_r) &&
+                      finite_nonneg(kmax_r) && (kmax_r >= kmin_r) && good && fits;
+#pragma unroll
+            for (int i = 0; i < N; ++i) ok = ok && (qr[i] >= 0.0 && qr[i] <= 1.0);
+            long long cur[MV];
+#pragma unroll
+            for (int v = 0; v < MV; ++v) cur[v] = 0;
+            uint8_t status = ok ? SPROUT_CELL_OK : SPROUT_CELL_INVALID;
+            if (ok) {
+                // Eq. 3 floor (lp_cell.cuh's formula and order) and k = ceil(fl(b * m))
+                double f = 0.0;
+                if (kmax_r > kmin_r) {
+                    f = __ddiv_rn(__dsub_rn(k0_s, kmin_r), __dsub_rn(kmax_r, kmin_r));
+                    f = f < 0.0 ? 0.0 : (f > 1.0 ? 1.0 : f);
+                }
+                const double b = __dmul_rn(__dsub_rn(1.0, __dmul_rn(f, xi)), qr[0]);
+                const double kk = ceil(__dmul_rn(b, (double)mreq));
+                int64_t need = (int64_t)kk - (int64_t)hit0;
+                if (need < 0) need = 0;
+                if (need > nc) { need = nc; status = SPROUT_CELL_INFEASIBLE; }
+                if (need > 0) {
+                    const int64_t owner = min((need - 1) / chunk, (int64_t)kOrThreads - 1);
+#pragma unroll
+                    for (int v = 0; v < MV; ++v) cur[v] = csum[(size_t)owner * MV + v];
+                    for (int64_t i = owner * chunk; i < need; ++i) apply(move[is[i]], cur);
+                }
+            }
+            a.cell_status_out[cell] = status;
+            double E = 0.0, Tm = 0.0, Q = 0.0;
+            for (int c = 0; c < NC; ++c) {
+#pragma unroll
+                for (int L = 0; L < N; ++L) {
+                    unsigned long long cn = 0ull, tk2 = 0ull;
+                    if (ok && c < NCM) {
+                        cn = (unsigned long long)((long long)tot[B_CNT + c * N + L] + cur[c * N + L]);
+                        tk2 = (unsigned long long)((long long)tot[B_TOK + c * N + L] + cur[NCM * N + c * N + L]);
+                    }
+                    a.cnt[(cell * NC + c) * N + L] = cn;
+                    a.tok[(cell * NC + c) * N + L] = tk2;
+                    const double n_ = (double)cn, t_ = (double)tk2;
+                    E += n_ * a.cost.ef[c][L] + t_ * a.cost.et[c][L];
+                    Tm += n_ * a.cost.pf[c][L] + t_ * a.cost.pt[c][L];
+                    Q += n_ * qr[L];
+                }
+            }
+            a.energy[cell] = E;
+            a.time_s[cell] = Tm;
+            a.carbon[cell] = ok ? __dmul_rn(k0_s, a.pue) * E + a.k1 * Tm : 0.0;
+            a.quality[cell] = Q;
+            a.stats[cell * 3 + 0] = ok ? (unsigned long long)((long long)hit0 + cur[2 * NCM * N]) : 0ull;
+            a.stats[cell * 3 + 1] = ok ? (unsigned long long)((long long)tot[B_WIN] + cur[2 * NCM * N + 1]) : 0ull;
+            a.stats[cell * 3 + 2] = ok ? (unsigned long long)((long long)tot[B_LOSS] + cur[2 * NCM * N + 2]) : 0ull;
+        }
+        if (tid == 0) {   // segment statistics and the Base counterfactual (write_seg_stats' formulas)
+            double bE = 0.0, bT = 0.0, mm = 0.0;
+            for (int c = 0; c < NC; ++c) {
+                const unsigned long long *ss = tot + S_BASE + (c < NCM ? c : 0) * (N + 2);
+                const unsigned long long mc = c < NCM ? ss[0] : 0ull;
+                a.seg_count[sl * NC + c] = mc;
+                a.seg_pinned[sl * NC + c] = c < NCM ? ss[1] : 0ull;
+                for (int L = 0; L < N; ++L) a.seg_tok[(sl * NC + c) * N + L] = c < NCM ? ss[2 + L] : 0ull;
+                const unsigned long long t0 = c < NCM ? ss[2] : 0ull;
+                bE += (double)mc * a.cost.ef[c][0] + (double)t0 * a.cost.et[c][0];
+                bT += (double)mc * a.cost.pf[c][0] + (double)t0 * a.cost.pt[c][0];
+                mm += (double)mc;
+            }
+            const double kp2 = a.k0[s] * a.pue;
+            a.seg_base[sl * 4 + 0] = bE;
+            a.seg_base[sl * 4 + 1] = bT;
+            a.seg_base[sl * 4 + 2] = kp2 * bE + a.k1 * bT;
+            a.seg_base[sl * 4 + 3] = mm * qr[0];
+        }
+        __syncthreads();
+    }
+    err = __reduce_or_sync(0xFFFFFFFFu, err);
+    if (lane == 0 && err) atomicOr(a.trace_status, err);
+}
+
+cudaError_t launch_oracle_scheme(N4Args &a, cudaStream_t stream, int *launches) {
+    round_keys(a);
+    if (cudaMemsetAsync(a.queue, 0, 4, stream) != cudaSuccess) return cudaErrorUnknown;
+    if (a.n_segments == 0) return cudaSuccess;
+    int64_t grid = sm_count();
+    if (grid > a.n_segments) grid = a.n_segments;
+#define OR_CASE(NN)                                                                                     \
+    case NN:                                                                                            \
+        if (a.NC > 1) oracle_scheme_kernel<NN, kMaxClasses><<<(unsigned)grid, kOrThreads, 0, stream>>>(a); \
+        else oracle_scheme_kernel<NN, 1><<<(unsigned)grid, kOrThreads, 0, stream>>>(a);                \
+        break;
+    switch (a.n) {
+        OR_CASE(1) OR_CASE(2) OR_CASE(3) OR_CASE(4) OR_CASE(5) OR_CASE(6) OR_CASE(7) OR_CASE(8)
+        default: return cudaErrorInvalidValue;
+    }
+#undef OR_CASE
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace sprout

@@ -368,6 +368,55 @@ sprout_status sprout_preference_stats(const sprout_lp_problem *problem, const sp
     return st;
 }
 
+size_t sprout_oracle_scheme_workspace_bytes(const sprout_lp_problem *problem, int64_t max_segment_requests) {
+    if (validate_problem(problem) != SPROUT_OK || max_segment_requests < 0 ||
+        max_segment_requests > ((int64_t)1 << 32))
+        return 0;
+    return oracle_scheme_workspace_bytes(max_segment_requests);
+}
+
+sprout_status sprout_simulate_oracle_scheme(const sprout_lp_problem *problem, const sprout_trace *trace,
+                                            const sprout_cost_model *cost, int64_t max_segment_requests,
+                                            const sprout_cell_totals *totals, uint64_t *stats, uint8_t *cell_status,
+                                            void *workspace, size_t workspace_bytes, sprout_stream stream) {
+    sprout_status st = validate_problem(problem);
+    if (st == SPROUT_OK) st = validate_trace(problem, trace);
+    if (st == SPROUT_OK) st = validate_cost(cost);
+    if (st == SPROUT_OK) st = validate_totals(problem, totals);
+    if (st != SPROUT_OK) return st;
+    if (max_segment_requests < 0 || max_segment_requests > ((int64_t)1 << 32)) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (problem->n_segments > 0 && (!stats || !cell_status || !aligned(stats, 8))) return SPROUT_ERR_INVALID_ARGUMENT;
+    if (!workspace || !aligned(workspace, 256) ||
+        workspace_bytes < oracle_scheme_workspace_bytes(max_segment_requests))
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    N4Args a{};
+    a.n = problem->n_levels; a.X = problem->n_xi; a.NC = cost->n_classes;
+    a.T = problem->n_intervals; a.first_segment = problem->first_segment; a.n_segments = problem->n_segments;
+    a.profile_per_interval = problem->profile_per_interval;
+    a.k0 = problem->k0; a.q = problem->q; a.k1 = problem->k1; a.pue = problem->pue;
+    a.xi = problem->xi; a.kmin = problem->k0_min; a.kmax = problem->k0_max;
+    a.n_requests = trace->n_requests; a.first_request = trace->first_request; a.seg_offsets = trace->seg_offsets;
+    a.tokens = trace->tokens; a.pitch = trace->plane_pitch; a.flags = trace->flags; a.seed = cost->seed;
+    std::memcpy(a.cost.ef, cost->ef, sizeof(cost->ef));
+    std::memcpy(a.cost.et, cost->et, sizeof(cost->et));
+    std::memcpy(a.cost.pf, cost->pf, sizeof(cost->pf));
+    std::memcpy(a.cost.pt, cost->pt, sizeof(cost->pt));
+    a.cap = max_segment_requests;
+    a.queue = static_cast<uint32_t *>(workspace);
+    a.scratch = static_cast<uint8_t *>(workspace) + 256;
+    a.stats = stats; a.cell_status_out = cell_status;
+    a.cnt = totals->cnt; a.tok = totals->tok; a.energy = totals->energy_kwh; a.time_s = totals->time_s;
+    a.carbon = totals->carbon_g; a.quality = totals->quality; a.seg_count = totals->seg_count;
+    a.seg_pinned = totals->seg_pinned; a.seg_tok = totals->seg_tok; a.seg_base = totals->seg_base;
+    a.trace_status = totals->trace_status;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaMemsetAsync(totals->trace_status, 0, 4, s) != cudaSuccess) return SPROUT_ERR_CUDA;
+    int launches = 0;
+    st = cuda_status(launch_oracle_scheme(a, s, &launches));
+    if (st == SPROUT_OK) g_last_launches = launches;
+    return st;
+}
+
 double sprout_normalized_preference(double w) {
     if (!(w >= 0.0)) return std::nan("");
     return w >= 1.0 ? HUGE_VAL : w / (1.0 - w);

@@ -99,6 +99,17 @@ struct N4Args {                 // NEXT-4 kernels (next4.cu)
     uint8_t *level_out, *pref_out;
     double *carbon_out, *base_out, *ratio_out;
     uint64_t *stats;           // [cells][3] hits, wins, losses
+    // the Oracle scheme (oracle_scheme_kernel)
+    const double *xi, *kmin, *kmax;
+    int64_t cap;               // max requests per segment (scratch per CTA)
+    uint8_t *scratch;          // [grid][32 * cap] bytes
+    uint8_t *cell_status_out;
+    uint64_t *cnt, *tok;
+    double *energy, *time_s, *carbon, *quality;
+    uint64_t *seg_count, *seg_pinned, *seg_tok;
+    double *seg_base;
+    uint32_t *trace_status;
+    uint32_t *queue;
 };
 
 struct EvalArgs {               // evaluator trigger sweep (evaluator.cu)
@@ -215,6 +226,8 @@ cudaError_t launch_evaluator(const EvalArgs &a, cudaStream_t stream, int *launch
 cudaError_t launch_closed_loop(ClosedArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_request_outputs(N4Args &a, cudaStream_t stream, int *launches);
 cudaError_t launch_pref_stats(N4Args &a, cudaStream_t stream, int *launches);
+cudaError_t launch_oracle_scheme(N4Args &a, cudaStream_t stream, int *launches);
+size_t oracle_scheme_workspace_bytes(int64_t cap);
 cudaError_t launch_select_static(const SelectArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_check_cells(const uint8_t *status, int64_t n_cells, uint32_t *out, cudaStream_t stream, int *launches);
 

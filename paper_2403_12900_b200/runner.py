@@ -125,6 +125,18 @@ class Sweep:
         S.preference_stats(self.dp, self.sol, self.trace, self.cost, st, stream)
         return st
 
+    def oracle_scheme(self, stream=None) -> dict:
+        """NEXT-4: the Oracle scheme into self.totals; returns stats and cell status."""
+        seg = self.trace.seg_offsets
+        cap = int((seg[1:] - seg[:-1]).max().item()) if seg.numel() > 1 else 0
+        if getattr(self, "_or_ws", None) is None or self._or_cap < cap:
+            self._or_cap = cap
+            self._or_ws = S.workspace(S.oracle_scheme_workspace_bytes(self.dp, cap), self.device)
+        st = torch.zeros((self.dp.cells, 3), dtype=torch.int64, device=self.device)
+        cs = torch.zeros(self.dp.cells, dtype=torch.uint8, device=self.device)
+        S.simulate_oracle_scheme(self.dp, self.trace, self.cost, self._or_cap, self.totals, st, cs, self._or_ws, stream)
+        return dict(stats=st, cell_status=cs)
+
     def reduce(self, stream=None):
         S.reduce_totals(self.dp, self.sol, self.totals, self.n_classes, self.group, self.rws, stream)
 

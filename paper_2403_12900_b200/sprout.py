@@ -28,7 +28,7 @@ MAX_LEVELS = 8
 MAX_CLASSES = 4
 MAX_XI = 4096
 CELL_OK, CELL_INVALID, CELL_INFEASIBLE = 0, 1, 2
-TRACE_BAD_CLASS, TRACE_BAD_OFFSETS, TRACE_SLOW_PATH = 0x1, 0x2, 0x100
+TRACE_BAD_CLASS, TRACE_BAD_OFFSETS, TRACE_TOO_LONG, TRACE_SLOW_PATH = 0x1, 0x2, 0x4, 0x100
 
 STATUS = {0: "SPROUT_OK", 1: "SPROUT_ERR_INVALID_ARGUMENT", 2: "SPROUT_ERR_INFEASIBLE",
           3: "SPROUT_ERR_OVERFLOW", 4: "SPROUT_ERR_CUDA", 5: "SPROUT_ERR_INVALID_CELL"}
@@ -125,7 +125,8 @@ EXPORTS = ["sprout_solve_directives", "sprout_workspace_bytes", "sprout_simulate
            "sprout_last_launch_count", "sprout_status_string", "sprout_solve_scheme", "sprout_static_grid_size",
            "sprout_select_static", "sprout_simulate_trace_bounded", "sprout_evaluator_sweep",
            "sprout_simulate_closed_loop", "sprout_request_outputs", "sprout_preference_stats",
-           "sprout_normalized_preference"]
+           "sprout_normalized_preference", "sprout_oracle_scheme_workspace_bytes",
+           "sprout_simulate_oracle_scheme"]
 
 # competing schemes, include/sprout.h SPROUT_SCHEME_*
 SCHEME_SPROUT, SCHEME_CO2_OPT, SCHEME_STATIC_GRID = 0, 1, 2
@@ -429,3 +430,24 @@ def preference_stats(prob: DeviceProblem, sol: Solution, trace: DeviceTrace, cos
 
 def normalized_preference(w: float) -> float:
     return float(_lib.sprout_normalized_preference(float(w)))
+
+
+_lib.sprout_oracle_scheme_workspace_bytes.argtypes = [_P(LpProblem), C.c_int64]
+_lib.sprout_oracle_scheme_workspace_bytes.restype = C.c_size_t
+_lib.sprout_simulate_oracle_scheme.argtypes = [_P(LpProblem), _P(Trace), _P(CostModel), C.c_int64, _P(CellTotals),
+                                               _vp, _vp, _vp, C.c_size_t, _vp]
+
+
+def oracle_scheme_workspace_bytes(prob: DeviceProblem, max_segment_requests: int) -> int:
+    p = prob.c()
+    return int(_lib.sprout_oracle_scheme_workspace_bytes(C.byref(p), int(max_segment_requests)))
+
+
+def simulate_oracle_scheme(prob: DeviceProblem, trace: DeviceTrace, cost: CostModel, max_segment_requests: int,
+                           totals: Totals, stats: torch.Tensor, cell_status: torch.Tensor, workspace: torch.Tensor,
+                           stream=None) -> None:
+    p, t, tt = prob.c(), trace.c(), totals.c()
+    _check("sprout_simulate_oracle_scheme",
+           _lib.sprout_simulate_oracle_scheme(C.byref(p), C.byref(t), C.byref(cost), int(max_segment_requests),
+                                              C.byref(tt), _ptr(stats), _ptr(cell_status), _ptr(workspace),
+                                              workspace.numel() * workspace.element_size(), _stream(stream)))

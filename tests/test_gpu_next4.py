@@ -55,3 +55,43 @@ def test_normalized_preference_host():
     assert S.normalized_preference(0.48) == pytest.approx(0.923, abs=1e-3)
     assert S.normalized_preference(0.5) == 1.0
     assert S.normalized_preference(1.0) == float("inf")
+
+
+@pytest.mark.parametrize("name,kw", [("C1", {}), ("C2", dict(n_requests=40_000, n_intervals=48)),
+                                     ("C3", dict(n_requests=30_000, n_intervals=96)),
+                                     ("C4", dict(n_requests=300_000, n_intervals=12)),
+                                     ("C5", dict(n_requests=30_000, n_intervals=24, n_regions=4))])
+def test_oracle_scheme_parity(name, kw):
+    w, sh, toks, fl, sw = _sweep(name, **kw)
+    res = sw.oracle_scheme()
+    torch.cuda.synchronize()
+    got = sw.host()
+    want = oracle.oracle_scheme(w.prob, w.cost, w.spec.seg_offsets, toks, fl)
+    NC, n = w.cost.n_classes, w.prob.n
+    np.testing.assert_array_equal(res["cell_status"].cpu().numpy(), want["status"])
+    np.testing.assert_array_equal(res["stats"].cpu().numpy().view(np.uint64), want["stats"])
+    np.testing.assert_array_equal(got["cnt"].reshape(-1, NC, n), want["cnt"])
+    np.testing.assert_array_equal(got["tok"].reshape(-1, NC, n), want["tok"])
+    for k in ("energy", "time", "carbon", "quality"):
+        np.testing.assert_allclose(got[k].reshape(-1), want[k], rtol=1e-9, atol=0, err_msg=k)
+    S_ = w.prob.R * w.prob.T
+    off = w.spec.seg_offsets
+    sim = oracle.simulate(w.prob, w.cost, np.arange(S_), off[:-1], np.diff(off), off[:-1], toks, fl)
+    np.testing.assert_array_equal(got["seg_count"].reshape(sim["seg_count"].shape), sim["seg_count"])
+    np.testing.assert_allclose(got["seg_base"].reshape(sim["seg_base"].shape), sim["seg_base"], rtol=1e-9, atol=0)
+    assert got["trace_status"] == 0
+
+
+def test_oracle_scheme_too_long_segment_flagged():
+    w, sh, toks, fl, sw = _sweep("C2", n_requests=20_000, n_intervals=24)
+    cap = 50   # shorter than most segments
+    ws = S.workspace(S.oracle_scheme_workspace_bytes(sw.dp, cap), sw.device)
+    st = torch.zeros((sw.dp.cells, 3), dtype=torch.int64, device=sw.device)
+    cs = torch.zeros(sw.dp.cells, dtype=torch.uint8, device=sw.device)
+    S.simulate_oracle_scheme(sw.dp, sw.trace, sw.cost, cap, sw.totals, st, cs, ws)
+    torch.cuda.synchronize()
+    got = sw.host()
+    assert got["trace_status"] & S.TRACE_TOO_LONG
+    m = np.diff(sh.seg_offsets)
+    long_ = np.repeat(m > cap, w.prob.X)
+    assert np.all(got["cnt"].reshape(len(long_), -1)[long_].sum(axis=1) == 0)
