@@ -117,17 +117,18 @@ def _bind(L):
     L.orc_head_to_head.argtypes = [C.c_int, C.c_int, _ip, _ip]
     L.orc_head_to_head.restype = None
     L.orc_preference.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
-                                 C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, _i64p, _u8p, C.c_int,
+                                 C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, _i64p, _u64p, _u8p, C.c_int,
                                  C.c_int, _u64p]
     L.orc_preference.restype = C.c_int
     L.orc_request_outputs.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
                                       C.c_int, C.c_double, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp, _dp,
-                                      _i64p, _u16p, C.c_int64, _u8p, C.c_int, C.c_int, C.c_int,
+                                      _i64p, _u64p, _u16p, C.c_int64, _u8p, C.c_int, C.c_int, C.c_int,
                                       _u8p, _dp, _dp, _dp, _u8p]
     L.orc_request_outputs.restype = C.c_int
     L.orc_oracle_scheme.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp, C.c_int,
                                     C.c_double, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp, _dp,
-                                    _i64p, _u16p, C.c_int64, _u8p, _u64p, _u64p, _dp, _dp, _dp, _dp, _u64p, _u8p]
+                                    _i64p, _u64p, _u16p, C.c_int64, _u8p, _u64p, _u64p, _dp, _dp, _dp, _dp, _u64p,
+                                    _u8p]
     L.orc_oracle_scheme.restype = C.c_int
     return L
 
@@ -408,21 +409,28 @@ def _problem_args(prob):
             _p(_f64(prob.q), _dp), int(prob.profile_per_interval), float(prob.k1), float(prob.pue))
 
 
-def preference(prob, cost, seg_offsets, flags=None, scheme: int = 0, grid_den: int = 0):
-    """Per cell [R*T*X][3]: hits (L = l*), wins, losses against Base (reading L22)."""
+def _g0(g0):
+    return None if g0 is None else np.ascontiguousarray(g0, dtype=np.uint64)
+
+
+def preference(prob, cost, seg_offsets, flags=None, scheme: int = 0, grid_den: int = 0, g0=None):
+    """Per cell [R*T*X][3]: hits (L = l*), wins, losses against Base (reading L22).
+    g0: per segment, the global index of its first request (default: seg_offsets)."""
     keep = [_f64(a) for a in (prob.k0, prob.kmin, prob.kmax, prob.xi, prob.e, prob.p, prob.q)]
     off = np.ascontiguousarray(seg_offsets, dtype=np.int64)
     fl = None if flags is None else np.ascontiguousarray(flags, dtype=np.uint8)
     out = np.zeros((prob.R * prob.T * prob.X, 3), np.uint64)
+    gb = _g0(g0)
     st = lib().orc_preference(*_problem_args(prob), C.c_uint64(int(cost.seed)), int(cost.n_classes),
-                              _p(off, _i64p), _p(fl, _u8p), int(scheme), int(grid_den), _p(out, _u64p))
+                              _p(off, _i64p), _p(gb, _u64p), _p(fl, _u8p), int(scheme), int(grid_den), _p(out, _u64p))
     del keep
     if st != 0:
         raise ValueError("oracle preference: invalid argument")
     return out
 
 
-def request_outputs(prob, cost, seg_offsets, tokens, flags=None, j: int = 0, scheme: int = 0, grid_den: int = 0):
+def request_outputs(prob, cost, seg_offsets, tokens, flags=None, j: int = 0, scheme: int = 0, grid_den: int = 0,
+                    g0=None):
     """Per request of cell column j: level, carbon, Base carbon, ratio (Fig. eval2), l*."""
     off = np.ascontiguousarray(seg_offsets, dtype=np.int64)
     tokens = np.ascontiguousarray(tokens, dtype=np.uint16)
@@ -433,7 +441,7 @@ def request_outputs(prob, cost, seg_offsets, tokens, flags=None, j: int = 0, sch
     ef, et, pf, pt = (_f64(a) for a in (cost.ef, cost.et, cost.pf, cost.pt))
     st = lib().orc_request_outputs(*_problem_args(prob), C.c_uint64(int(cost.seed)), int(cost.n_classes),
                                    _p(ef, _dp), _p(et, _dp), _p(pf, _dp), _p(pt, _dp), _p(off, _i64p),
-                                   _p(tokens, _u16p), tokens.shape[1], _p(fl, _u8p), int(scheme), int(grid_den),
+                                   _p(_g0(g0), _u64p), _p(tokens, _u16p), tokens.shape[1], _p(fl, _u8p), int(scheme), int(grid_den),
                                    int(j), _p(out["level"], _u8p), _p(out["carbon"], _dp), _p(out["base"], _dp),
                                    _p(out["ratio"], _dp), _p(out["pref"], _u8p))
     if st != 0:
@@ -441,7 +449,7 @@ def request_outputs(prob, cost, seg_offsets, tokens, flags=None, j: int = 0, sch
     return out
 
 
-def oracle_scheme(prob, cost, seg_offsets, tokens, flags=None):
+def oracle_scheme(prob, cost, seg_offsets, tokens, flags=None, g0=None):
     """The Oracle scheme (reading L23), per cell: cnt/tok [NC][n],
     energy/time/carbon/quality sums, stats (hits, wins, losses), status."""
     n, R, T, X, NC = prob.n, prob.R, int(prob.T), prob.X, cost.n_classes
@@ -457,8 +465,8 @@ def oracle_scheme(prob, cost, seg_offsets, tokens, flags=None):
                                  _p(_f64(prob.kmax), _dp), _p(_f64(prob.xi), _dp), _p(_f64(prob.q), _dp),
                                  int(prob.profile_per_interval), float(prob.k1), float(prob.pue),
                                  C.c_uint64(int(cost.seed)), NC, _p(ef, _dp), _p(et, _dp), _p(pf, _dp), _p(pt, _dp),
-                                 _p(off, _i64p), _p(tokens, _u16p), tokens.shape[1], _p(fl, _u8p),
-                                 _p(out["cnt"], _u64p), _p(out["tok"], _u64p), _p(out["energy"], _dp),
+                                 _p(off, _i64p), _p(_g0(g0), _u64p), _p(tokens, _u16p), tokens.shape[1],
+                                 _p(fl, _u8p), _p(out["cnt"], _u64p), _p(out["tok"], _u64p), _p(out["energy"], _dp),
                                  _p(out["time"], _dp), _p(out["carbon"], _dp), _p(out["quality"], _dp),
                                  _p(out["stats"], _u64p), _p(out["status"], _u8p))
     if st != 0:

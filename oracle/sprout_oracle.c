@@ -924,13 +924,14 @@ void orc_head_to_head(int L, int lstar, int *win, int *loss)
  * mix, a6): stats[cell][0..2] = hits (L = l*, the realised Eq. 3 left-hand
  * side), wins, losses against Base.  Requests with an invalid class and
  * invalid cells are skipped.  Arguments as orc_simulate_scheme (all R*T
- * segments; request g = global index).                                      */
+ * segments); requests indexed by seg_offsets, global index g0[s] + (i -
+ * seg_offsets[s]) (g0 NULL: the index itself).                              */
 int orc_preference(int n, int R, int64_t T, int X,
                    const double *k0, const double *kmin, const double *kmax, const double *xi,
                    const double *e, const double *p, const double *q, int profile_per_interval,
                    double k1, double pue, uint64_t seed, int n_classes,
-                   const int64_t *seg_offsets, const uint8_t *flags, int scheme, int grid_den,
-                   uint64_t *stats)
+                   const int64_t *seg_offsets, const uint64_t *g0, const uint8_t *flags, int scheme,
+                   int grid_den, uint64_t *stats)
 {
     if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1) return 1;
     if (n_classes < 1 || n_classes > ORC_MAX_CLASSES) return 1;
@@ -945,12 +946,13 @@ int orc_preference(int n, int R, int64_t T, int X,
             uint64_t *st = stats + ((size_t)s * X + j) * 3;
             st[0] = st[1] = st[2] = 0;
             if (solve_cell(&P, s, j, xs, &obj, &qlb, &vid, Tl, &ml) != 0) continue;
-            for (int64_t g = seg_offsets[s]; g < seg_offsets[s + 1]; ++g) {
+            for (int64_t i = seg_offsets[s]; i < seg_offsets[s + 1]; ++i) {
+                const uint64_t g = g0 ? g0[s] + (uint64_t)(i - seg_offsets[s]) : (uint64_t)i;   /* global index */
                 int pinned = 0, cls = 0;
-                if (flags) { pinned = flags[g] & 1; cls = (flags[g] >> 1) & 3; }
+                if (flags) { pinned = flags[i] & 1; cls = (flags[i] >> 1) & 3; }
                 if (cls >= n_classes) continue;
-                const int L = orc_select_level(n, xs, orc_draw_word(seed, (uint64_t)g), pinned);
-                const int ls = orc_pref_level(n, qs, seed, (uint64_t)g);
+                const int L = orc_select_level(n, xs, orc_draw_word(seed, g), pinned);
+                const int ls = orc_pref_level(n, qs, seed, g);
                 int win, loss;
                 orc_head_to_head(L, ls, &win, &loss);
                 st[0] += (uint64_t)(L == ls);
@@ -973,7 +975,7 @@ int orc_request_outputs(int n, int R, int64_t T, int X,
                         const double *e, const double *p, const double *q, int profile_per_interval,
                         double k1, double pue, uint64_t seed, int n_classes,
                         const double *ef, const double *et, const double *pf, const double *pt,
-                        const int64_t *seg_offsets, const uint16_t *tokens, int64_t pitch,
+                        const int64_t *seg_offsets, const uint64_t *g0, const uint16_t *tokens, int64_t pitch,
                         const uint8_t *flags, int scheme, int grid_den, int j,
                         uint8_t *level, double *carbon, double *base, double *ratio, uint8_t *pref)
 {
@@ -988,22 +990,23 @@ int orc_request_outputs(int n, int R, int64_t T, int X,
         const int ok = solve_cell(&P, s, j, xs, &obj, &qlb, &vid, Tl, &ml) == 0;
         const double kp = P.k0[s] * pue;
         const double *qs = prof(&P, q, s);
-        for (int64_t g = seg_offsets[s]; g < seg_offsets[s + 1]; ++g) {
+        for (int64_t i = seg_offsets[s]; i < seg_offsets[s + 1]; ++i) {
+            const uint64_t g = g0 ? g0[s] + (uint64_t)(i - seg_offsets[s]) : (uint64_t)i;   /* global index */
             int pinned = 0, cls = 0;
-            if (flags) { pinned = flags[g] & 1; cls = (flags[g] >> 1) & 3; }
-            pref[g] = (uint8_t)orc_pref_level(n, qs, seed, (uint64_t)g);
+            if (flags) { pinned = flags[i] & 1; cls = (flags[i] >> 1) & 3; }
+            pref[i] = (uint8_t)orc_pref_level(n, qs, seed, g);
             if (!ok || cls >= n_classes) {
-                level[g] = 0xFF; carbon[g] = NAN; base[g] = NAN; ratio[g] = NAN;
+                level[i] = 0xFF; carbon[i] = NAN; base[i] = NAN; ratio[i] = NAN;
                 continue;
             }
-            const int L = orc_select_level(n, xs, orc_draw_word(seed, (uint64_t)g), pinned);
-            const double tl = (double)tokens[(size_t)L * pitch + g], t0 = (double)tokens[g];
+            const int L = orc_select_level(n, xs, orc_draw_word(seed, g), pinned);
+            const double tl = (double)tokens[(size_t)L * pitch + i], t0 = (double)tokens[i];
             const double el = ef[cls * 8 + L] + et[cls * 8 + L] * tl, pl = pf[cls * 8 + L] + pt[cls * 8 + L] * tl;
             const double e0 = ef[cls * 8] + et[cls * 8] * t0, p0 = pf[cls * 8] + pt[cls * 8] * t0;
-            level[g] = (uint8_t)L;
-            carbon[g] = orc_request_carbon(kp, k1, el, pl);
-            base[g] = orc_request_carbon(kp, k1, e0, p0);
-            ratio[g] = carbon[g] / base[g];
+            level[i] = (uint8_t)L;
+            carbon[i] = orc_request_carbon(kp, k1, el, pl);
+            base[i] = orc_request_carbon(kp, k1, e0, p0);
+            ratio[i] = carbon[i] / base[i];
         }
     }
     return 0;
@@ -1040,8 +1043,8 @@ int orc_oracle_scheme(int n, int R, int64_t T, int X,
                       const double *q, int profile_per_interval, double k1, double pue,
                       uint64_t seed, int n_classes, const double *ef, const double *et,
                       const double *pf, const double *pt,
-                      const int64_t *seg_offsets, const uint16_t *tokens, int64_t pitch, const uint8_t *flags,
-                      uint64_t *cnt, uint64_t *tok, double *energy, double *time_s, double *carbon,
+                      const int64_t *seg_offsets, const uint64_t *gbase, const uint16_t *tokens, int64_t pitch,
+                      const uint8_t *flags, uint64_t *cnt, uint64_t *tok, double *energy, double *time_s, double *carbon,
                       double *quality, uint64_t *stats, uint8_t *status)
 {
     if (n < 1 || n > ORC_MAX_LEVELS || R < 1 || T < 1 || X < 1) return 1;
@@ -1059,7 +1062,8 @@ int orc_oracle_scheme(int n, int R, int64_t T, int X,
         orc_cand *cand = (orc_cand *)malloc(sizeof(orc_cand) * (size_t)(m_all > 0 ? m_all : 1));
         int64_t m = 0, free_hits = 0, nc = 0;
         for (int64_t i = 0; i < m_all; ++i) {
-            const int64_t g = g0 + i;
+            const int64_t g = g0 + i;                                            /* local index */
+            const uint64_t gg = gbase ? gbase[s] + (uint64_t)i : (uint64_t)g;   /* global index */
             int pinned = 0, c = 0;
             if (flags) { pinned = flags[g] & 1; c = (flags[g] >> 1) & 3; }
             cls[i] = c;
@@ -1073,7 +1077,7 @@ int orc_oracle_scheme(int n, int R, int64_t T, int X,
             int best = 0;
             for (int L = 1; L < n; ++L) if (C[L] < C[best]) best = L;
             lm[i] = best;
-            ls[i] = orc_pref_level(n, qs, seed, (uint64_t)g);
+            ls[i] = orc_pref_level(n, qs, seed, gg);
             ch[i] = pinned ? 0 : best;
             free_hits += (ch[i] == ls[i]);
             if (!pinned && ls[i] != best) {

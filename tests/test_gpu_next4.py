@@ -95,3 +95,64 @@ def test_oracle_scheme_too_long_segment_flagged():
     m = np.diff(sh.seg_offsets)
     long_ = np.repeat(m > cap, w.prob.X)
     assert np.all(got["cnt"].reshape(len(long_), -1)[long_].sum(axis=1) == 0)
+
+
+def _sample_subproblem(w, ids):
+    """The sampled segments as a compact problem (one 'region' per segment,
+    T = 1) with their requests regenerated on the host; g0 = each segment's
+    global first request (the Philox counters)."""
+    import dataclasses
+    P = w.prob
+    regs = np.asarray(ids) // P.T
+    sub = dataclasses.replace(P, R=len(ids), T=1, k0=np.asarray(P.k0)[ids], kmin=np.asarray(P.kmin)[regs],
+                              kmax=np.asarray(P.kmax)[regs], e=np.asarray(P.e)[regs], p=np.asarray(P.p)[regs],
+                              q=np.asarray(P.q)[regs])
+    parts, fparts, off = [], [], [0]
+    for s in ids:
+        a, b = int(w.spec.seg_offsets[s]), int(w.spec.seg_offsets[s + 1])
+        t, f = synth.gen_tokens(w.spec, a, b)
+        parts.append(t); fparts.append(f); off.append(off[-1] + b - a)
+    toks = np.concatenate(parts, axis=1)
+    fl = np.concatenate(fparts) if w.spec.has_flags else None
+    return sub, np.array(off, np.int64), toks, fl, np.asarray(w.spec.seg_offsets)[ids].astype(np.uint64)
+
+
+def test_next4_full_size_c4_sampled():
+    """C4 at full size (10^9 requests generated on the GPU): the Oracle scheme,
+    the head-to-head statistics and one xi column's per-request outputs on a
+    deterministic sample of segments (every 997th + first/last/largest)
+    against the oracle run on those segments alone."""
+    w = synth.make_workload("C4")
+    sh = synth.shard(w.spec, 1, 0)
+    sw = Sweep(w.prob, w.cost, sh, DEV, spec=w.spec)
+    sw.solve()
+    pref = sw.preference_stats().cpu().numpy().view(np.uint64)
+    j = 40
+    ro = sw.request_outputs(j)
+    orr = sw.oracle_scheme()
+    torch.cuda.synchronize()
+    got = sw.host()
+    assert got["trace_status"] == 0
+    ids = synth.sample_segments(w.spec, 0, sh.n_segments, every=997)
+    sub, off, toks, fl, g0 = _sample_subproblem(w, ids)
+    X, NC, n = w.prob.X, w.cost.n_classes, w.prob.n
+    cidx = (np.asarray(ids)[:, None] * X + np.arange(X)[None, :]).reshape(-1)
+    # head-to-head statistics
+    want = oracle.preference(sub, w.cost, off, fl, g0=g0)
+    np.testing.assert_array_equal(pref[cidx], want)
+    # per-request outputs of column j
+    wr = oracle.request_outputs(sub, w.cost, off, toks, fl, j=j, g0=g0)
+    for k, (s, a0) in enumerate(zip(ids, off[:-1])):
+        a, b = int(w.spec.seg_offsets[s]), int(w.spec.seg_offsets[s + 1])
+        sl = slice(a, b)
+        np.testing.assert_array_equal(ro["level"][sl].cpu().numpy(), wr["level"][a0:a0 + b - a])
+        np.testing.assert_array_equal(ro["pref"][sl].cpu().numpy(), wr["pref"][a0:a0 + b - a])
+        np.testing.assert_array_equal(ro["ratio"][sl].cpu().numpy().view(np.uint64),
+                                      wr["ratio"][a0:a0 + b - a].view(np.uint64))
+    # the Oracle scheme
+    wo = oracle.oracle_scheme(sub, w.cost, off, toks, fl, g0=g0)
+    np.testing.assert_array_equal(orr["cell_status"].cpu().numpy()[cidx], wo["status"])
+    np.testing.assert_array_equal(orr["stats"].cpu().numpy().view(np.uint64)[cidx], wo["stats"])
+    np.testing.assert_array_equal(got["cnt"].reshape(-1, NC, n)[cidx], wo["cnt"])
+    np.testing.assert_array_equal(got["tok"].reshape(-1, NC, n)[cidx], wo["tok"])
+    np.testing.assert_allclose(got["carbon"].reshape(-1)[cidx], wo["carbon"], rtol=1e-9, atol=0)
