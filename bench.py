@@ -46,7 +46,7 @@ def peaks():
 
 def workload_desc(w, scheme="sprout"):
     P = w.prob
-    cells = {"sprout": "xi", "co2opt": "CO2_Opt cell", "static": "static grid points"}[scheme]
+    cells = {"sprout": "xi", "co2opt": "CO2_Opt cell", "static": "static grid points", "oracle": "xi (Oracle scheme)"}[scheme]
     return (f"{w.name}: {P.R} regions x {P.T} CI intervals x {P.X} {cells} x {P.n} directive levels, "
             f"{w.N:,} requests, {w.cost.n_classes} model class(es), flags={'yes' if w.spec.has_flags else 'no'}")
 
@@ -214,7 +214,7 @@ def run_reference(args):
 # ---------------------------------------------------------------- GPU arm
 
 
-SCHEMES = {"sprout": 0, "co2opt": 1, "static": 2}
+SCHEMES = {"sprout": 0, "co2opt": 1, "static": 2, "oracle": 3}   # oracle: NEXT-4's Oracle scheme
 
 
 def scheme_workload(args):
@@ -224,7 +224,7 @@ def scheme_workload(args):
     import dataclasses
     import math
     w = synth.make_workload(args.config)
-    if args.scheme == "sprout":
+    if args.scheme in ("sprout", "oracle"):
         return w
     X = 1 if args.scheme == "co2opt" else math.comb(args.grid_den + w.prob.n - 1, w.prob.n - 1)
     prob = dataclasses.replace(w.prob, X=X, xi=np.zeros(X))
@@ -287,7 +287,10 @@ def run_sprout(args):
     scheme = SCHEMES[args.scheme]
     # closed-loop chains are per region: ranks take whole regions; otherwise request-balanced segments
     sh = synth.shard_regions(w.spec, w.prob.T, world, rank) if args.closed_loop else synth.shard(w.spec, world, rank)
-    sw = Sweep(w.prob, w.cost, sh, dev, spec=w.spec, scheme=scheme, grid_den=args.grid_den)
+    oracle_scheme = args.scheme == "oracle"
+    sw = Sweep(w.prob, w.cost, sh, dev, spec=w.spec, scheme=0 if oracle_scheme else scheme, grid_den=args.grid_den)
+    if oracle_scheme:   # the Sprout LP once: every cell's status for the reduction (the Oracle has no mix)
+        sw.solve()
     stream = torch.cuda.current_stream()
     torch.cuda.synchronize()
     trace_bytes = sw.trace.tokens.numel() * 2 + (sw.trace.flags.numel() if sw.trace.flags is not None else 0)
@@ -298,12 +301,14 @@ def run_sprout(args):
     launches = [0]
 
     def step(ev=None):
-        if not args.closed_loop:   # the closed-loop scan solves every interval's LP itself
+        if not args.closed_loop and not oracle_scheme:   # the closed-loop scan solves every interval's LP itself
             sw.solve(); launches[0] += S.last_launch_count()
         if ev is not None:
             ev[0].record(stream)
         if args.closed_loop:
             sw.closed_loop(args.closed_loop); launches[0] += S.last_launch_count()
+        elif oracle_scheme:
+            sw.oracle_scheme(); launches[0] += S.last_launch_count()
         else:
             sw.simulate(); launches[0] += S.last_launch_count()
         if ev is not None:
@@ -355,6 +360,38 @@ def run_sprout(args):
     status = int(sw.totals.trace_status.item())
     g = sw.group.cpu().numpy()
 
+    # NEXT-4 reporting (untimed by the step; each kernel timed on its own)
+    extras = {}
+    if args.preference and not args.closed_loop:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if oracle_scheme:
+            e0.record(stream); st = sw.oracle_scheme()["stats"]; e1.record(stream)
+        else:
+            e0.record(stream); st = sw.preference_stats(); e1.record(stream)
+        torch.cuda.synchronize()
+        st = st.view(sh.n_segments, w.prob.X, 3).sum(dim=0).double().cpu().numpy()
+        m = float(w.N)
+        pick = sorted({0, w.prob.X // 2, w.prob.X - 1})
+        extras["preference"] = {
+            "reading": "L22: head-to-head vs Base, ties half; score = w/(1-w) (P:377)",
+            "kernel_ms": e0.elapsed_time(e1),
+            "by_xi": [{"xi": float(w.prob.xi[j]), "hit_rate": st[j, 0] / m,
+                       "w": (st[j, 1] + (m - st[j, 1] - st[j, 2]) / 2) / m,
+                       "normalized_preference": S.normalized_preference((st[j, 1] + (m - st[j, 1] - st[j, 2]) / 2) / m)}
+                      for j in pick]}
+    if args.request_cdf >= 0 and not args.closed_loop and not oracle_scheme:
+        j = min(args.request_cdf, w.prob.X - 1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream); ro = sw.request_outputs(j); e1.record(stream)
+        torch.cuda.synchronize()
+        r = ro["ratio"]
+        r = r[~torch.isnan(r)]
+        edges = [0.1 * k for k in range(1, 11)]
+        extras["request_cdf"] = {"xi": float(w.prob.xi[j]), "kernel_ms": e0.elapsed_time(e1),
+                                 "requests": int(r.numel()),
+                                 "fraction_at_or_below": {f"{x:.1f}": float((r <= x).double().mean().item()) for x in edges}}
+        del ro, r
+
     # e2e: the host-buffer C-ABI call (H2D of the trace + D2H of the totals timed)
     e2e = None
     if not args.no_e2e and scheme == S.SCHEME_SPROUT and not args.closed_loop:
@@ -379,7 +416,7 @@ def run_sprout(args):
         key = f"{w.name}/{args.scheme}/{'closed' if args.closed_loop else 'open'}/{world}"
         traffic = json.load(open(tf)).get(key, {}).get("dram_bytes_per_launch")
     cpu = None
-    if not args.no_cpu_baseline and world == 1 and not args.closed_loop:
+    if not args.no_cpu_baseline and world == 1 and not args.closed_loop and not oracle_scheme:
         cpu = oracle_baseline(w, args.cpu_seconds, scheme, args.grid_den)
     N = w.N
     line = {
@@ -397,7 +434,9 @@ def run_sprout(args):
         "request_cells_per_s": N * w.prob.X / (ms_per_step * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": ("sprout_simulate_closed_loop (one CTA per group of xi chains "
-                                                    "of a region)" if args.closed_loop
+                                                    "of a region)" if args.closed_loop else
+                                                    "sprout_simulate_oracle_scheme (one CTA per segment: per-request "
+                                                    "costs, radix sort by extra carbon)" if oracle_scheme
                                                     else "sprout_simulate_trace (prep + trace_kernel, CUDA events)"),
                      "algorithmic_bytes_per_launch": alg, "launch_ms": sim_avg_ms, "peak_source": peak_src},
         "clocks": clk.summary(),
@@ -405,6 +444,7 @@ def run_sprout(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "trace_status": status,
+        **extras,
         "check": {"requests_counted": float(g[-1, 0, 0]),
                   "carbon_saving_xi_max": float(1 - g[-1, -1, 4] / g[-1, -1, 8]) if g[-1, -1, 8] > 0 else None},
     }
@@ -488,6 +528,10 @@ def main():
     ap.add_argument("--static-xi", type=float, default=0.1, help="xi of the Sprout_Sta quality floor")
     ap.add_argument("--closed-loop", type=int, default=0, metavar="W",
                     help="closed-loop profiles (NEXT-1): window of W requests per level; 0 = open loop")
+    ap.add_argument("--preference", action="store_true",
+                    help="NEXT-4: head-to-head preference vs Base per xi (reading L22, P:377) after the timed steps")
+    ap.add_argument("--request-cdf", type=int, default=-1, metavar="J",
+                    help="NEXT-4: per-request carbon / Base of xi column J (Fig. eval2 CDF points) after the timed steps")
     ap.add_argument("--evaluator", action="store_true",
                     help="time the opportunistic evaluator trigger sweep (Eq. 8) instead of the hot path")
     args = ap.parse_args()
