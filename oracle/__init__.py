@@ -104,10 +104,13 @@ def _bind(L):
                                       C.c_double, C.c_int, C.c_double, C.c_double, _dp]
     L.orc_evaluator_sweep.restype = C.c_int
     L.orc_closed_loop.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
-                                  C.c_double, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp, _dp, C.c_int,
+                                  C.c_double, C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp, _dp, C.c_int, _dp,
                                   _i64p, _u16p, C.c_int64, _u8p, _dp, _u64p, _u8p, _dp, _dp, _u64p, _u64p, _dp, _dp,
                                   _dp, _dp]
     L.orc_closed_loop.restype = C.c_int
+    L.orc_evaluation_q.argtypes = [C.c_int, C.c_int64, C.c_double, _dp, _dp, C.c_double, C.c_double, C.c_double,
+                                   C.c_int, C.c_int, _dp, C.c_uint64, _i64p, C.c_int, _dp, _u8p]
+    L.orc_evaluation_q.restype = C.c_int
     L.orc_pref_word.argtypes = [C.c_uint64, C.c_uint64]
     L.orc_pref_word.restype = C.c_uint32
     L.orc_pref_level.argtypes = [C.c_int, _dp, C.c_uint64, C.c_uint64]
@@ -348,7 +351,7 @@ def evaluator_sweep(k2, k2max, T: int, dt: float, betas, thetas, grace: float, f
     return out
 
 
-def closed_loop(prob, cost, window: int, seg_offsets, tokens, flags=None):
+def closed_loop(prob, cost, window: int, seg_offsets, tokens, flags=None, q_seg=None):
     """Closed-loop profiles (NEXT-1): per (region, xi) chain, the LP of
     each interval uses the mean E and T of the last `window` requests run at
     each level.  Requests are global: tokens [n][pitch] indexed by the global
@@ -369,7 +372,8 @@ def closed_loop(prob, cost, window: int, seg_offsets, tokens, flags=None):
                                _p(_f64(prob.kmax), _dp), _p(_f64(prob.xi), _dp), _p(_f64(prob.e), _dp),
                                _p(_f64(prob.p), _dp), _p(_f64(prob.q), _dp), float(prob.k1), float(prob.pue),
                                C.c_uint64(int(cost.seed)), NC, _p(ef, _dp), _p(et, _dp), _p(pf, _dp), _p(pt, _dp),
-                               int(window), _p(off, _i64p), _p(tokens, _u16p), tokens.shape[1], _p(fl, _u8p),
+                               int(window), _p(None if q_seg is None else _f64(q_seg), _dp),
+                               _p(off, _i64p), _p(tokens, _u16p), tokens.shape[1], _p(fl, _u8p),
                                _p(out["x"], _dp), _p(out["threshold"], _u64p), _p(out["cell_status"], _u8p),
                                _p(out["objective"], _dp), _p(out["profile"], _dp), _p(out["cnt"], _u64p), _p(out["tok"], _u64p), _p(out["energy"], _dp),
                                _p(out["time"], _dp), _p(out["carbon"], _dp), _p(out["quality"], _dp))
@@ -472,3 +476,19 @@ def oracle_scheme(prob, cost, seg_offsets, tokens, flags=None, g0=None):
     if st != 0:
         raise ValueError("oracle oracle_scheme: invalid argument")
     return out
+
+
+def evaluation_q(k2, k2max, T: int, dt: float, beta: float, theta: float, grace: float, fallback: int, q_true,
+                 seed: int, seg_offsets, sample: int = 500):
+    """NEXT-1 q update (reading L24): (q per interval [R*T][n], fired [R*T])."""
+    k2 = _f64(k2); k2max = _f64(k2max); q_true = _f64(q_true)
+    R = len(k2max)
+    n = q_true.shape[-1]
+    off = np.ascontiguousarray(seg_offsets, dtype=np.int64)
+    q_out = np.zeros((R * T, n)); fired = np.zeros(R * T, np.uint8)
+    st = lib().orc_evaluation_q(R, int(T), float(dt), _p(k2, _dp), _p(k2max, _dp), float(beta), float(theta),
+                                float(grace), int(fallback), int(n), _p(q_true, _dp), C.c_uint64(int(seed)),
+                                _p(off, _i64p), int(sample), _p(q_out, _dp), _p(fired, _u8p))
+    if st != 0:
+        raise ValueError("oracle evaluation_q: invalid argument")
+    return q_out, fired

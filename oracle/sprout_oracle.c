@@ -777,7 +777,9 @@ int orc_evaluator_sweep(int R, int64_t T, double dt, const double *k2, const dou
  * per-class request counts n_c and token sums k_c (exact integers):
  *   e_L = (sum_c (n_c*ef[c][L] + k_c*et[c][L])) / (sum_c n_c),
  * summed in class order (p_L likewise with pf, pt).  The LP of the interval
- * (solve_cell with these e, p and the region's q) gives x and thresholds;
+ * (solve_cell with these e, p and the region's q -- or interval s's row of
+ * q_seg when given: the q of its evaluation epoch, reading L24) gives x and
+ * thresholds;
  * then the interval's requests are replayed as in orc_simulate and pushed,
  * in request order, into their level's window.  Outputs per cell
  * (r*T + t)*X + j: the solution and the cell totals.  Requests: global
@@ -786,7 +788,7 @@ int orc_closed_loop(int n, int R, int64_t T, int X,
                     const double *k0, const double *kmin, const double *kmax, const double *xi,
                     const double *e_prior, const double *p_prior, const double *q, double k1, double pue,
                     uint64_t seed, int n_classes, const double *ef, const double *et,
-                    const double *pf, const double *pt, int W,
+                    const double *pf, const double *pt, int W, const double *q_seg,
                     const int64_t *seg_offsets, const uint16_t *tokens, int64_t pitch, const uint8_t *flags,
                     double *x_out, uint64_t *thr_out, uint8_t *status_out, double *obj_out, double *prof_out,
                     uint64_t *cnt, uint64_t *tok, double *energy, double *time_s, double *carbon, double *quality)
@@ -827,8 +829,9 @@ int orc_closed_loop(int n, int R, int64_t T, int X,
                     prof_out[(cell * 2 + 1) * n + L] = p[L];
                 }
                 /* the interval's LP with the closed-loop profile */
+                const double *qs = q_seg ? &q_seg[(size_t)s * n] : &q[(size_t)r * n];   /* L24: q per epoch */
                 orc_problem P = { n, R, 1, 0, NC, 1, &k0[s], &kmin[r], &kmax[r], &xi[j], e, p,
-                                  &q[(size_t)r * n], k1, pue, ORC_SCHEME_SPROUT, 0 };
+                                  qs, k1, pue, ORC_SCHEME_SPROUT, 0 };
                 double xs[ORC_MAX_LEVELS], obj, qlb; int vid, ml; uint64_t Tl[ORC_MAX_LEVELS];
                 int st = solve_cell(&P, 0, 0, xs, &obj, &qlb, &vid, Tl, &ml);
                 obj_out[cell] = obj;
@@ -850,7 +853,7 @@ int orc_closed_loop(int n, int R, int64_t T, int X,
                         const uint32_t tl = tokens[(size_t)L * pitch + g];
                         const double el = ef[cls * 8 + L] + et[cls * 8 + L] * (double)tl;
                         const double pl = pf[cls * 8 + L] + pt[cls * 8 + L] * (double)tl;
-                        E += el; Tm += pl; Cb += orc_request_carbon(kp, k1, el, pl); Q += q[(size_t)r * n + L];
+                        E += el; Tm += pl; Cb += orc_request_carbon(kp, k1, el, pl); Q += qs[L];
                         cn[cls * n + L] += 1; tk[cls * n + L] += tl;
                         /* push into level L's window (FIFO of the last W) */
                         int slot = head[L];
@@ -1128,6 +1131,74 @@ int orc_oracle_scheme(int n, int R, int64_t T, int X,
             energy[cell] = E; time_s[cell] = Tm; carbon[cell] = Cb; quality[cell] = Q;
         }
         free(moved); free(cls); free(lm); free(ls); free(ch); free(cand);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-1's q update per evaluation epoch (reading L24).  An
+ * evaluation offers "a timely update to the q^T vector": the
+ * evaluator samples 500 requests, generates every level's response
+ * and records the best level of each; q is their preference rates
+ * (P:190).  For region r and ONE evaluator configuration (beta, theta, grace,
+ * fallback), the evaluations fire at the intervals of the trigger scan of
+ * orc_evaluator_sweep (Eq. 8, reading L19; the trace start counts as one).
+ * An evaluation at interval t samples the last `sample` requests of the
+ * region before interval t starts (all of them if fewer; none: q unchanged)
+ * and sets q_i = #{l* = i} / #sampled (the latent best level of reading L21,
+ * drawn against the region's true q row q_true); that q holds from interval t
+ * until the next evaluation.  Before any evaluation with samples, q is
+ * q_true.  Outputs: q_out [R*T][n], fired [R*T] (1 where an evaluation
+ * fired, t = 0 included).  seg_offsets [R*T+1] global request indices.     */
+int orc_evaluation_q(int R, int64_t T, double dt, const double *k2, const double *k2max, double beta,
+                     double theta, double grace, int F, int n, const double *q_true, uint64_t seed,
+                     const int64_t *seg_offsets, int sample, double *q_out, uint8_t *fired)
+{
+    if (R < 1 || T < 1 || F < 0 || !(dt > 0.0) || n < 1 || n > ORC_MAX_LEVELS || sample < 1) return 1;
+    for (int r = 0; r < R; ++r) {
+        const double *k = k2 + (int64_t)r * T;
+        const double *qt = q_true + (size_t)r * n;
+        const double d = exp(-(beta * dt));
+        const double thr = theta * k2max[r];
+        double qc[ORC_MAX_LEVELS];
+        for (int i = 0; i < n; ++i) qc[i] = qt[i];
+        /* the trigger scan (orc_evaluator_sweep's state and rules) */
+        int64_t t0 = 0, below = 0;
+        double f = 1.0, prev1 = k[0], prev2 = 0.0;
+        for (int64_t t = 0; t < T; ++t) {
+            int fire = t == 0;
+            if (t > 0) {
+                f = f * d;
+                double kp = f * k[t];
+                int under = kp < thr;
+                if (under) below = below + 1; else below = 0;
+                int64_t since = t - t0;
+                int grace_ok = (double)since * dt >= grace;
+                int local_min = since >= 2 && prev1 < prev2 && kp > prev1;
+                int fallback = F > 0 && below >= F;
+                prev2 = prev1;
+                prev1 = kp;
+                if (grace_ok && under && (local_min || fallback)) {
+                    fire = 1;
+                    t0 = t;
+                    f = 1.0;
+                    prev1 = k[t];
+                    below = 0;
+                }
+            }
+            const int64_t s = (int64_t)r * T + t;
+            fired[s] = (uint8_t)fire;
+            if (fire) {
+                const int64_t region0 = seg_offsets[(int64_t)r * T], end = seg_offsets[s];
+                const int64_t begin = end - sample > region0 ? end - sample : region0;
+                if (end > begin) {
+                    int64_t cnt[ORC_MAX_LEVELS] = { 0 };
+                    for (int64_t g = begin; g < end; ++g) cnt[orc_pref_level(n, qt, seed, (uint64_t)g)] += 1;
+                    for (int i = 0; i < n; ++i) qc[i] = (double)cnt[i] / (double)(end - begin);
+                }
+            }
+            for (int i = 0; i < n; ++i) q_out[(size_t)s * n + i] = qc[i];
+        }
     }
     return 0;
 }
