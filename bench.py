@@ -306,7 +306,10 @@ def run_sprout(args):
         if ev is not None:
             ev[0].record(stream)
         if args.closed_loop:
-            sw.closed_loop(args.closed_loop); launches[0] += S.last_launch_count()
+            qi = None
+            if args.q_update:   # NEXT-1: q per evaluation epoch (Eq. 8 trigger, 500 samples; reading L24)
+                qi, _ = sw.evaluation_q(24.0 / (w.prob.T / 365), 0.028, 0.5, 6.0, 3, 500); launches[0] += 1
+            sw.closed_loop(args.closed_loop, q_interval=qi); launches[0] += S.last_launch_count()
         elif oracle_scheme:
             sw.oracle_scheme(); launches[0] += S.last_launch_count()
         else:
@@ -423,7 +426,8 @@ def run_sprout(args):
         "metric": METRIC, "value": N / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64/u32", "data": "synthetic",
-        "config": {"workload": workload_desc(w, args.scheme) + (f" [closed loop, window {args.closed_loop}]"
+        "config": {"workload": workload_desc(w, args.scheme) + (f" [closed loop, window {args.closed_loop}"
+                                                                   f"{', q per evaluation epoch' if args.q_update else ''}]"
                                                                    if args.closed_loop else ""),
                    "config": w.name, "scheme": args.scheme, "closed_loop_window": args.closed_loop, "requests": N,
                    "lp_cells": w.prob.C,
@@ -528,6 +532,8 @@ def main():
     ap.add_argument("--static-xi", type=float, default=0.1, help="xi of the Sprout_Sta quality floor")
     ap.add_argument("--closed-loop", type=int, default=0, metavar="W",
                     help="closed-loop profiles (NEXT-1): window of W requests per level; 0 = open loop")
+    ap.add_argument("--q-update", action="store_true",
+                    help="with --closed-loop: q updated per evaluation epoch (NEXT-1, reading L24) inside each step")
     ap.add_argument("--preference", action="store_true",
                     help="NEXT-4: head-to-head preference vs Base per xi (reading L22, P:377) after the timed steps")
     ap.add_argument("--request-cdf", type=int, default=-1, metavar="J",

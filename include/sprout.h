@@ -450,6 +450,34 @@ sprout_status sprout_simulate_oracle_scheme(const sprout_lp_problem *problem, co
  * fraction w in [0, 1] (+inf at w = 1; NaN for w < 0 or NaN).  Host. */
 double sprout_normalized_preference(double w);
 
+/* NEXT-1's q update per evaluation epoch (reading L24).  An evaluation
+ * offers "a timely update to the q^T vector": it samples 500 requests
+ * and records the best level of each.  For ONE evaluator
+ * configuration (ev: n_beta = n_theta = 1; k2 = the CI per region and
+ * interval, as in sprout_evaluator_sweep) the evaluations fire where the
+ * trigger scan of Eq. 8 fires (reading L19; t = 0 counts).  An evaluation
+ * at interval t samples the last `sample` requests of the region before
+ * interval t (all if fewer; none: q unchanged) and sets q_i = #{l* = i} /
+ * #sampled, l* the latent best level (reading L21) against the region's row
+ * of problem->q (the truth); that q holds from t until the next evaluation.
+ * problem must be the whole sweep (first_segment 0, n_segments = R*T,
+ * profile_per_interval 0).  Outputs (device): q_out [R*T][n] fp64 -- the q
+ * of every interval's epoch, e.g. for sprout_simulate_closed_loop_q --, and
+ * fired_out [R*T] u8 (1 at an evaluation).  One CTA per region.  Errors:
+ * INVALID_ARGUMENT; CUDA. */
+sprout_status sprout_evaluation_q(const sprout_evaluator_problem *ev, const sprout_lp_problem *problem,
+                                  const sprout_trace *trace, const sprout_cost_model *cost, int32_t sample,
+                                  double *q_out, uint8_t *fired_out, sprout_stream stream);
+
+/* sprout_simulate_closed_loop with the LP's q taken per interval from
+ * q_interval [R*T][n] (device; global segment index; NULL: problem->q per
+ * region) -- the closed loop with the q of each evaluation epoch (NEXT-1,
+ * reading L24).  Quality sums use the same rows. */
+sprout_status sprout_simulate_closed_loop_q(const sprout_lp_problem *problem, int32_t window, const double *q_interval,
+                                            const sprout_trace *trace, const sprout_cost_model *cost,
+                                            const sprout_lp_solution *solution, const sprout_cell_totals *totals,
+                                            double *profile_out, sprout_stream stream);
+
 /* Number of kernel launches (not memsets) the last successful call of each
  * entry point on this thread enqueued -- for launch accounting in benches. */
 int32_t sprout_last_launch_count(void);

@@ -162,6 +162,16 @@ sprout_status sprout_select_static(const sprout_lp_problem *problem, int32_t gri
     return st;
 }
 
+// the grace test in samples: the least s with (double)s * dt >= grace (the same decision for every s)
+static int64_t grace_samples(double grace_hours, double interval_hours) {
+    double s0 = std::ceil(grace_hours / interval_hours);
+    if (s0 > 2147483647.0) s0 = 2147483647.0;
+    int64_t s = (int64_t)s0;
+    while (s > 0 && (double)(s - 1) * interval_hours >= grace_hours) --s;
+    while (s < 2147483647 && !((double)s * interval_hours >= grace_hours)) ++s;
+    return s;
+}
+
 sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *P, double *out, sprout_stream stream) {
     if (!P || !out) return SPROUT_ERR_INVALID_ARGUMENT;
     if (P->n_regions < 1 || P->n_intervals < 1 || P->n_beta < 1 || P->n_beta > SPROUT_MAX_EVAL_PARAMS ||
@@ -174,14 +184,7 @@ sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *P, double *
     if (!P->k2 || !P->k2_max || !P->beta || !P->theta || !aligned(out, 8)) return SPROUT_ERR_INVALID_ARGUMENT;
     if (P->n_intervals >= ((int64_t)1 << 31)) return SPROUT_ERR_OVERFLOW;
     EvalArgs a{};
-    {   // grace test in samples: the least s with (double)s * dt >= grace (same decision for every s)
-        double s0 = std::ceil(P->grace_hours / P->interval_hours);
-        if (s0 > 2147483647.0) s0 = 2147483647.0;
-        int64_t s = (int64_t)s0;
-        while (s > 0 && (double)(s - 1) * P->interval_hours >= P->grace_hours) --s;
-        while (s < 2147483647 && !((double)s * P->interval_hours >= P->grace_hours)) ++s;
-        a.grace_samples = (int)s;
-    }
+    a.grace_samples = (int)grace_samples(P->grace_hours, P->interval_hours);
     a.R = P->n_regions; a.B = P->n_beta; a.H = P->n_theta; a.F = P->fallback; a.T = P->n_intervals;
     a.dt = P->interval_hours; a.grace = P->grace_hours; a.eval_kwh = P->eval_kwh; a.pue = P->pue;
     a.k2 = P->k2; a.k2_max = P->k2_max; a.out = out;
@@ -204,6 +207,14 @@ sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int3
                                           const sprout_trace *trace, const sprout_cost_model *cost,
                                           const sprout_lp_solution *solution, const sprout_cell_totals *totals,
                                           double *profile_out, sprout_stream stream) {
+    return sprout_simulate_closed_loop_q(problem, window, nullptr, trace, cost, solution, totals, profile_out, stream);
+}
+
+sprout_status sprout_simulate_closed_loop_q(const sprout_lp_problem *problem, int32_t window, const double *q_interval,
+                                            const sprout_trace *trace, const sprout_cost_model *cost,
+                                            const sprout_lp_solution *solution, const sprout_cell_totals *totals,
+                                            double *profile_out, sprout_stream stream) {
+    if (q_interval && !aligned(q_interval, 8)) return SPROUT_ERR_INVALID_ARGUMENT;
     sprout_status st = validate_problem(problem);
     if (st == SPROUT_OK) st = validate_solution(problem, solution);
     if (st == SPROUT_OK) st = validate_trace(problem, trace);
@@ -228,6 +239,7 @@ sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int3
     a.R_local = (int)(problem->n_segments / problem->n_intervals);
     a.k0 = problem->k0; a.kmin = problem->k0_min; a.kmax = problem->k0_max; a.xi = problem->xi;
     a.e = problem->e; a.p = problem->p; a.q = problem->q; a.k1 = problem->k1; a.pue = problem->pue;
+    a.q_seg = q_interval;
     {
         uint32_t k0 = (uint32_t)cost->seed, k1 = (uint32_t)(cost->seed >> 32);
         for (int r = 0; r < 10; ++r) { a.rk0[r] = k0; a.rk1[r] = k1; k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
@@ -413,6 +425,39 @@ sprout_status sprout_simulate_oracle_scheme(const sprout_lp_problem *problem, co
     if (cudaMemsetAsync(totals->trace_status, 0, 4, s) != cudaSuccess) return SPROUT_ERR_CUDA;
     int launches = 0;
     st = cuda_status(launch_oracle_scheme(a, s, &launches));
+    if (st == SPROUT_OK) g_last_launches = launches;
+    return st;
+}
+
+sprout_status sprout_evaluation_q(const sprout_evaluator_problem *ev, const sprout_lp_problem *problem,
+                                  const sprout_trace *trace, const sprout_cost_model *cost, int32_t sample,
+                                  double *q_out, uint8_t *fired_out, sprout_stream stream) {
+    sprout_status st = validate_problem(problem);
+    if (st == SPROUT_OK) st = validate_trace(problem, trace);
+    if (st == SPROUT_OK) st = validate_cost(cost);
+    if (st != SPROUT_OK) return st;
+    if (!ev || ev->n_beta != 1 || ev->n_theta != 1 || !ev->beta || !ev->theta || !ev->k2 || !ev->k2_max ||
+        ev->fallback < 0 || ev->n_regions != problem->n_regions || ev->n_intervals != problem->n_intervals)
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    if (!(ev->interval_hours > 0.0) || !std::isfinite(ev->interval_hours) || !(ev->grace_hours >= 0.0) ||
+        !std::isfinite(ev->grace_hours) || !(ev->beta[0] >= 0.0) || !std::isfinite(ev->beta[0]) ||
+        !(ev->theta[0] >= 0.0) || !std::isfinite(ev->theta[0]))
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    // the whole sweep (every region's intervals in order), q per region (the truth behind l*)
+    if (problem->first_segment != 0 || problem->n_segments != (int64_t)problem->n_regions * problem->n_intervals ||
+        problem->profile_per_interval != 0 || sample < 1 || !q_out || !fired_out || !aligned(q_out, 8))
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    EvalQArgs a{};
+    a.R = problem->n_regions; a.n = problem->n_levels; a.F = ev->fallback; a.sample = sample;
+    a.T = problem->n_intervals;
+    a.grace_samples = grace_samples(ev->grace_hours, ev->interval_hours);
+    a.decay = std::exp(-(ev->beta[0] * ev->interval_hours));   // Eq. 8's factor over one interval (reading L19)
+    a.theta = ev->theta[0];
+    a.k2 = ev->k2; a.k2_max = ev->k2_max; a.q = problem->q;
+    a.seg_offsets = trace->seg_offsets; a.first_request = trace->first_request; a.seed = cost->seed;
+    a.q_out = q_out; a.fired = fired_out;
+    int launches = 0;
+    st = cuda_status(launch_evaluation_q(a, reinterpret_cast<cudaStream_t>(stream), &launches));
     if (st == SPROUT_OK) g_last_launches = launches;
     return st;
 }

@@ -123,6 +123,18 @@ struct EvalArgs {               // evaluator trigger sweep (evaluator.cu)
     double *out;               // [R][B][H][4]
 };
 
+struct EvalQArgs {              // q per evaluation epoch (evaluator.cu)
+    int R, n, F, sample;
+    int64_t T, grace_samples;
+    double decay, theta;       // exp(-beta * dt) (host), theta as a fraction of k2_max
+    const double *k2, *k2_max, *q;   // q: true rows [R][n]
+    const int64_t *seg_offsets;      // [R*T+1] local
+    uint64_t first_request, seed;
+    uint32_t rk0[10], rk1[10];
+    double *q_out;             // [R*T][n]
+    uint8_t *fired;            // [R*T]
+};
+
 struct SelectArgs {            // Sprout_Sta choice per region (schemes.cu)
     int n, R, G, K, grid_den;
     int64_t T;
@@ -225,6 +237,7 @@ cudaError_t launch_generate(const GenArgs &a, cudaStream_t stream, int *launches
 cudaError_t launch_evaluator(const EvalArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_closed_loop(ClosedArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_request_outputs(N4Args &a, cudaStream_t stream, int *launches);
+cudaError_t launch_evaluation_q(EvalQArgs &a, cudaStream_t stream, int *launches);
 cudaError_t launch_pref_stats(N4Args &a, cudaStream_t stream, int *launches);
 cudaError_t launch_oracle_scheme(N4Args &a, cudaStream_t stream, int *launches);
 size_t oracle_scheme_workspace_bytes(int64_t cap);

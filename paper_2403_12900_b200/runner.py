@@ -99,15 +99,27 @@ class Sweep:
         else:
             S.simulate_trace(self.dp, self.sol, self.trace, self.cost, self.totals, self.ws, lv, stream)
 
-    def closed_loop(self, window: int, profile: bool = False, stream=None):
+    def closed_loop(self, window: int, profile: bool = False, q_interval: Optional[torch.Tensor] = None, stream=None):
         """Closed-loop profiles (NEXT-1): steps 1-2 as a causal scan per
         (region, xi) chain; writes the solution and every totals field
-        (cells and segments), so reduce() can follow directly."""
+        (cells and segments), so reduce() can follow directly.  q_interval
+        [R*T][n]: the q of every interval's evaluation epoch (evaluation_q)."""
         prof = None
         if profile:
             prof = torch.zeros((self.dp.cells, 2, self.prob_host.n), dtype=torch.float64, device=self.device)
-        S.simulate_closed_loop(self.dp, window, self.trace, self.cost, self.sol, self.totals, prof, stream)
+        S.simulate_closed_loop_q(self.dp, window, q_interval, self.trace, self.cost, self.sol, self.totals, prof, stream)
         return prof
+
+    def evaluation_q(self, interval_hours: float, beta: float, theta: float, grace_hours: float, fallback: int,
+                     sample: int = 500, stream=None):
+        """NEXT-1: q per evaluation epoch (reading L24) -> (q [R*T][n], fired [R*T])."""
+        P = self.prob_host
+        k2 = self.dp.k0
+        q = torch.zeros((P.R * P.T, P.n), dtype=torch.float64, device=self.device)
+        fired = torch.zeros(P.R * P.T, dtype=torch.uint8, device=self.device)
+        S.evaluation_q(self.dp, self.trace, self.cost, k2, self.dp.kmax, interval_hours, beta, theta, grace_hours,
+                       fallback, sample, q, fired, stream)
+        return q, fired
 
     def request_outputs(self, xi_index: int, stream=None) -> dict:
         """NEXT-4: per-request level, carbon, Base carbon, ratio and latent best level of one xi column."""

@@ -126,7 +126,7 @@ EXPORTS = ["sprout_solve_directives", "sprout_workspace_bytes", "sprout_simulate
            "sprout_select_static", "sprout_simulate_trace_bounded", "sprout_evaluator_sweep",
            "sprout_simulate_closed_loop", "sprout_request_outputs", "sprout_preference_stats",
            "sprout_normalized_preference", "sprout_oracle_scheme_workspace_bytes",
-           "sprout_simulate_oracle_scheme"]
+           "sprout_simulate_oracle_scheme", "sprout_evaluation_q", "sprout_simulate_closed_loop_q"]
 
 # competing schemes, include/sprout.h SPROUT_SCHEME_*
 SCHEME_SPROUT, SCHEME_CO2_OPT, SCHEME_STATIC_GRID = 0, 1, 2
@@ -451,3 +451,32 @@ def simulate_oracle_scheme(prob: DeviceProblem, trace: DeviceTrace, cost: CostMo
            _lib.sprout_simulate_oracle_scheme(C.byref(p), C.byref(t), C.byref(cost), int(max_segment_requests),
                                               C.byref(tt), _ptr(stats), _ptr(cell_status), _ptr(workspace),
                                               workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+# NEXT-1: q per evaluation epoch (reading L24) and the closed loop with it
+_lib.sprout_evaluation_q.argtypes = [_P(EvaluatorProblem), _P(LpProblem), _P(Trace), _P(CostModel), C.c_int32,
+                                     _vp, _vp, _vp]
+_lib.sprout_simulate_closed_loop_q.argtypes = [_P(LpProblem), C.c_int32, _vp, _P(Trace), _P(CostModel),
+                                               _P(LpSolution), _P(CellTotals), _vp, _vp]
+
+
+def evaluation_q(prob: DeviceProblem, trace: DeviceTrace, cost: CostModel, k2: torch.Tensor, k2_max: torch.Tensor,
+                 interval_hours: float, beta: float, theta: float, grace_hours: float, fallback: int, sample: int,
+                 q_out: torch.Tensor, fired_out: torch.Tensor, stream=None) -> None:
+    b = np.array([beta], np.float64)
+    t = np.array([theta], np.float64)
+    E = EvaluatorProblem(int(k2_max.numel()), 1, int(prob.T), float(interval_hours), _ptr(k2), _ptr(k2_max),
+                         b.ctypes.data, 1, int(fallback), t.ctypes.data, float(grace_hours), 0.0, 1.0)
+    p, tr = prob.c(), trace.c()
+    _check("sprout_evaluation_q",
+           _lib.sprout_evaluation_q(C.byref(E), C.byref(p), C.byref(tr), C.byref(cost), int(sample), _ptr(q_out),
+                                    _ptr(fired_out), _stream(stream)))
+
+
+def simulate_closed_loop_q(prob: DeviceProblem, window: int, q_interval: Optional[torch.Tensor], trace: DeviceTrace,
+                           cost: CostModel, sol: Solution, totals: Totals, profile_out: Optional[torch.Tensor] = None,
+                           stream=None) -> None:
+    p, t, s, tt = prob.c(), trace.c(), sol.c(), totals.c()
+    _check("sprout_simulate_closed_loop_q",
+           _lib.sprout_simulate_closed_loop_q(C.byref(p), int(window), _ptr(q_interval), C.byref(t), C.byref(cost),
+                                              C.byref(s), C.byref(tt), _ptr(profile_out), _stream(stream)))

@@ -132,3 +132,32 @@ def test_closed_loop_bad_offsets():
     want = oracle.closed_loop(w.prob, w.cost, 50, w.spec.seg_offsets, toks, fl)
     lo, hi = T * X, 2 * T * X
     np.testing.assert_array_equal(got["cnt"].reshape(-1, NC, n)[lo:hi], want["cnt"][lo:hi])
+
+
+@pytest.mark.parametrize("name,kw,dt,grace,sample", [("C2", dict(n_requests=60_000, n_intervals=240), 1.0, 6.0, 500),
+                                                     ("C3", dict(n_requests=40_000, n_intervals=288, n_regions=2),
+                                                      1 / 12, 2.0, 500),
+                                                     ("C4", dict(n_requests=200_000, n_intervals=96), 1.0, 6.0, 37)])
+def test_evaluation_q_and_closed_loop_q(name, kw, dt, grace, sample):
+    """NEXT-1's q update (reading L24): every interval's epoch q and the
+    evaluation flags bit-exact; the closed loop with those q bit-exact."""
+    w = synth.make_workload(name, **kw)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, fl = synth.host_trace(w.spec, sh)
+    P = w.prob
+    sw = Sweep(P, w.cost, sh, DEV, tokens=toks, flags=fl)
+    q, fired = sw.evaluation_q(dt, 0.028, 0.5, grace, 3, sample)
+    prof = sw.closed_loop(100, profile=True, q_interval=q)
+    torch.cuda.synchronize()
+    got = sw.host()
+    wq, wf = oracle.evaluation_q(P.k0, P.kmax, P.T, dt, 0.028, 0.5, grace, 3, np.asarray(P.q), w.cost.seed,
+                                 w.spec.seg_offsets, sample)
+    np.testing.assert_array_equal(fired.cpu().numpy(), wf)
+    np.testing.assert_array_equal(q.cpu().numpy().view(np.uint64), wq.view(np.uint64))
+    want = oracle.closed_loop(P, w.cost, 100, w.spec.seg_offsets, toks, fl, q_seg=wq)
+    NC, n = w.cost.n_classes, P.n
+    np.testing.assert_array_equal(prof.cpu().numpy().view(np.uint64), want["profile"].view(np.uint64))
+    np.testing.assert_array_equal(got["x"].view(np.uint64), want["x"].view(np.uint64))
+    np.testing.assert_array_equal(got["cnt"].reshape(-1, NC, n), want["cnt"])
+    np.testing.assert_allclose(got["quality"].reshape(-1), want["quality"], rtol=FP_RTOL, atol=0)
+    np.testing.assert_allclose(got["carbon"].reshape(-1), want["carbon"], rtol=FP_RTOL, atol=0)
