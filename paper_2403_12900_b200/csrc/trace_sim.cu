@@ -383,7 +383,7 @@ __device__ __forceinline__ void build_lut(const WarpSmem &W, int K, LutGeom g, u
         const uint32_t key = W.keys[j];
         const uint32_t b = (key - g.base) >> g.s;
         atomicAdd(&W.lut[b].y, 1u);
-        W.lut[b].x = key;   // meaningful only when the bucket holds exactly one key
+        atomicExch(&W.lut[b].x, key);   // meaningful only when the bucket holds exactly one key (else replaced below)
     }
     __syncwarp();
     const uint32_t lt = (1u << lane) - 1u;
