@@ -169,10 +169,15 @@ def oracle_baseline(w, target_s=12.0, scheme=0, grid_den=0):
     every = max(1, int(np.ceil(w.N / max(want, 1))))
     ids = synth.sample_segments(w.spec, 0, S, every=every)
     req, nseg, dt = oracle_sample_run(w, ids, threads, scheme, grid_den)
+    # one thread: the first segments of the same sample, ~target_s / 4 of CPU
+    n1 = max(1, int(len(ids) * min(1.0, (target_s / 4) / max(dt * threads, 1e-6))))
+    req1, nseg1, dt1 = oracle_sample_run(w, ids[:n1], 1, scheme, grid_den)
     return {"value": req / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{nseg} whole segments (every {every}th + first/last/largest) = {req:,} requests x "
                       f"{w.prob.X} xi cells, LP solves included, token generation excluded; {dt:.2f} s",
-            "lp_cells_per_s": nseg * w.prob.X / dt}
+            "lp_cells_per_s": nseg * w.prob.X / dt,
+            "one_thread": {"value": req1 / dt1, "unit": UNIT, "cores": 1,
+                           "sample": f"the first {nseg1} segments of that sample = {req1:,} requests; {dt1:.2f} s"}}
 
 
 def run_reference(args):
@@ -326,6 +331,12 @@ def run_sprout(args):
             flush_buf.zero_()
         step()
     torch.cuda.synchronize()
+    graph = None
+    if args.graph:   # the whole step (all its launches + the all-reduce) as one CUDA graph replay
+        graph = sw.capture(step)
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches[0] = 0
@@ -340,13 +351,22 @@ def run_sprout(args):
             if flush:
                 flush_buf.zero_()       # L2 flush between steps (outside the per-step events)
             step_ev[k][0].record(stream)
-            step(sim_ev[k])
+            if graph is not None:
+                graph.replay()
+            else:
+                step(sim_ev[k])
             step_ev[k][1].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    if graph is not None:   # the simulate launch alone, eagerly, for the roofline
+        for k in range(args.steps):
+            if flush:
+                flush_buf.zero_()
+            step(sim_ev[k])
+        torch.cuda.synchronize()
     sim_ms = [a.elapsed_time(b) for a, b in sim_ev]
     total_ms = max_over_ranks(sum(step_ms), dev)
     ms_per_step = total_ms / args.steps
@@ -412,6 +432,7 @@ def run_sprout(args):
         f = 1 if w.spec.has_flags else 0
         alg = algorithmic_bytes(w, sh) + sh.n_segments * P.X * (P.n * 8 + 8 + 8)
     sim_avg_ms = statistics.mean(sim_ms)
+    sim_med_ms = statistics.median(sim_ms)
     achieved = alg / (sim_avg_ms * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
@@ -424,7 +445,8 @@ def run_sprout(args):
     N = w.N
     line = {
         "metric": METRIC, "value": N / (ms_per_step * 1e-3), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "ms_per_step_median": statistics.median(step_ms), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64/u32", "data": "synthetic",
         "config": {"workload": workload_desc(w, args.scheme) + (f" [closed loop, window {args.closed_loop}"
                                                                    f"{', q per evaluation epoch' if args.q_update else ''}]"
@@ -432,6 +454,7 @@ def run_sprout(args):
                    "config": w.name, "scheme": args.scheme, "closed_loop_window": args.closed_loop, "requests": N,
                    "lp_cells": w.prob.C,
                    "parallelism": f"segments sharded over {world} GPU(s), one NCCL allreduce of group totals",
+                   "cuda_graph": bool(args.graph),
                    "l2": ("flushed (256 MB memset) between steps" if flush else
                           f"inputs larger than L2 (trace {trace_bytes / 1e9:.2f} GB/GPU > L2 {l2 / 1e6:.0f} MB)")},
         "lp_cells_per_s": w.prob.C / (lp_ms * 1e-3),
@@ -442,7 +465,8 @@ def run_sprout(args):
                                                     "sprout_simulate_oracle_scheme (one CTA per segment: per-request "
                                                     "costs, radix sort by extra carbon)" if oracle_scheme
                                                     else "sprout_simulate_trace (prep + trace_kernel, CUDA events)"),
-                     "algorithmic_bytes_per_launch": alg, "launch_ms": sim_avg_ms, "peak_source": peak_src},
+                     "algorithmic_bytes_per_launch": alg, "launch_ms": sim_avg_ms, "launch_ms_median": sim_med_ms,
+                     "frac_median": alg / (sim_med_ms * 1e-3) / 1e9 / peak, "peak_source": peak_src},
         "clocks": clk.summary(),
         "gpu_launches": launches[0],
         "e2e": e2e,
@@ -532,6 +556,8 @@ def main():
     ap.add_argument("--static-xi", type=float, default=0.1, help="xi of the Sprout_Sta quality floor")
     ap.add_argument("--closed-loop", type=int, default=0, metavar="W",
                     help="closed-loop profiles (NEXT-1): window of W requests per level; 0 = open loop")
+    ap.add_argument("--graph", action="store_true",
+                    help="replay the step as one captured CUDA graph (runner.Sweep.capture)")
     ap.add_argument("--q-update", action="store_true",
                     help="with --closed-loop: q updated per evaluation epoch (NEXT-1, reading L24) inside each step")
     ap.add_argument("--preference", action="store_true",

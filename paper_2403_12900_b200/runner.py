@@ -157,6 +157,24 @@ class Sweep:
         self.simulate(False, stream)
         self.reduce(stream)
 
+    def capture(self, fn=None) -> "torch.cuda.CUDAGraph":
+        """Capture one step (default: solve -> simulate -> reduce; or `fn`, e.g.
+        one that adds the all-reduce) into a CUDA graph: the library launches
+        only asynchronous work on the given stream and allocates nothing, so
+        every later replay re-runs the whole step with one launch from the
+        host.  Buffers stay the ones of this Sweep."""
+        fn = fn or self.step
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):   # warm the lazy state (function attributes) outside the capture
+            fn()
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        return g
+
     # host views (for tests)
     def host(self) -> dict:
         t = self.totals

@@ -442,3 +442,28 @@ def test_x1_pure_mix_skips_draws(xi):
     # xi = 0: pure L0 (no draw needed); xi = 1 at high intensity: a pure or an edge mix per segment
     w = _custom(n=5, X=1, N=60_000, T=30, R=2, xi=[xi])
     check_full(w)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_graph_captured_step_matches_eager(world):
+    """The step captured in a CUDA graph (runner.Sweep.capture) and replayed
+    gives the eager step's results bit for bit, per shard (partition
+    invariance holds through the graph)."""
+    w = synth.make_workload("C4", n_requests=300_000, n_intervals=24)
+    for rank in range(world):
+        sh = synth.shard(w.spec, world, rank)
+        eager = Sweep(w.prob, w.cost, sh, DEV, spec=w.spec)
+        eager.step()
+        torch.cuda.synchronize()
+        want = eager.host()
+        sw = Sweep(w.prob, w.cost, sh, DEV, spec=w.spec)
+        g = sw.capture()
+        for k in ("cnt", "tok", "carbon", "energy"):
+            getattr(sw.totals, k).zero_()
+        g.replay(); g.replay()
+        torch.cuda.synchronize()
+        got = sw.host()
+        for k in ("cnt", "tok", "seg_count", "seg_tok"):
+            np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+        for k in ("energy", "time", "carbon", "quality", "group"):
+            np.testing.assert_array_equal(got[k].view(np.uint64), want[k].view(np.uint64), err_msg=k)
