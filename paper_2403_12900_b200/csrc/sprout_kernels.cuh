@@ -194,6 +194,11 @@ struct SimArgs {
     int lut;                   // 1: per-warp bucket table (kLutBuckets entries) for big segments
     size_t warp_smem;
     uint32_t rk0[10], rk1[10]; // Philox round keys of the selection seed
+    // trace_wide_kernel: Philox rounds 0-2 of a counter (lo, H, 0, 0) whose high
+    // word H is constant over the launch (see trace_sim.cu philox_lo)
+    uint32_t ph_a, ph_blo, ph_d, ph_e;
+    unsigned long long *wide_scratch;   // [warps][kcap+1][4] 64-bit spill rows
+    int wide;                  // 1: the launch runs trace_wide_kernel
     FastDiv div_nt;            // by n - 1 (thresholds per cell)
     FastDiv div_t;             // by T (region of a segment), valid when T < 2^32
     int seg_batch;             // segments per queue ticket

@@ -1475,6 +1475,711 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
 }
 
 // ---------------------------------------------------------------------------
+// trace_wide_kernel -- A/B EXPERIMENT, off by default (SPROUT_ENABLE_WIDE=1
+// to build it in): measured 2.62 ms (mbarrier ring, token loads from global)
+// and 3.88 ms (token planes TMA-staged through the ring) against
+// trace_kernel's 2.08 ms on C4 (profiles/r02_c4_experiments.md).  A
+// streaming kernel for n = 3 levels, one model class
+// and no flags plane (the C4 xi sweep, the Sprout_Sta grid sweep).  Same
+// method, histogram row format and epilogue as trace_kernel (a5-a8: one
+// draw per request shared by the segment's cells, reading L10; the bin
+// histogram; per-cell statistics from its prefix sums and Eq. 1 in closed
+// form), warp-specialised:
+//  * a TEAM of two warps owns one segment at a time.  The PRODUCER warp
+//    computes each request's Philox word and its histogram row (bucket
+//    table over the fixed range [0, 2^32), exact bin by binary search for the
+//    rare draws in buckets holding several keys) and writes the rows into a
+//    ring of shared-memory stages; the CONSUMER warp streams the token planes
+//    (128-bit loads, L2 prefetch) and does the serial read-modify-writes of
+//    its lane-private rows.  mbarriers (full / empty per stage) pace the ring.
+//    The producer holds no histogram, so 8 teams (16 warps, 4 per scheduler)
+//    fit in shared memory where trace_kernel fits 8 warps: the consumers'
+//    load-latency-bound chains interleave with the producers' integer rounds;
+//  * rows whose guard bits are set spill into a per-team 64-bit scratch in
+//    global memory (rare); after the stream the table space holds the 64-bit
+//    rows that the shared epilogue (cell_epilogue, write_seg_stats) reads;
+//  * Philox rounds 0-2 are specialised on the counter's constant words
+//    (c1 = H, constant over the launch; c2 = c3 = 0).
+#ifndef SPROUT_WIDE_TEAMS
+#define SPROUT_WIDE_TEAMS 7
+#endif
+#ifndef SPROUT_WIDE_LB
+#define SPROUT_WIDE_LB 9
+#endif
+#ifndef SPROUT_WIDE_STAGES
+#define SPROUT_WIDE_STAGES 4
+#endif
+#ifndef SPROUT_ENABLE_WIDE
+#define SPROUT_ENABLE_WIDE 0   // A/B only: measured slower than trace_kernel on C4 (profiles/r02_c4_experiments.md)
+#endif
+#ifndef SPROUT_WIDE_AB_NOPHILOX
+#define SPROUT_WIDE_AB_NOPHILOX 0   // A/B timing only (wrong results)
+#endif
+#ifndef SPROUT_WIDE_PREFETCH
+#define SPROUT_WIDE_PREFETCH 3
+#endif
+constexpr int kWideTeams = SPROUT_WIDE_TEAMS;
+constexpr int kWideLB = SPROUT_WIDE_LB;
+constexpr int kWideBuckets = 1 << kWideLB;
+constexpr int kWideShift = 32 - kWideLB;
+constexpr int kWideStages = SPROUT_WIDE_STAGES;
+constexpr int kWideMaxSMs = 256;   // the spill scratch is sized for this many SMs
+// the table space must also hold the epilogue's 64-bit rows: (kcap + 3) * 4 * 8 <= kWideBuckets * 8
+constexpr int kWideMaxKeys = (kWideBuckets / 4 - 3) < 253 ? (kWideBuckets / 4 - 3) : 253;
+constexpr int kWideCtl = (16 * SPROUT_WIDE_STAGES + 48 + 127) / 128 * 128;   // per team: mbarriers full[S], empty[S], the segment record
+// a ring stage: 256 u32 histogram row addresses (16-byte chunks h*32 + lane), then the
+// iteration's three token planes (512 B each, copied by TMA bulk copies)
+constexpr int kWideStageBytes = 1024 + 3 * 512;
+#ifndef SPROUT_WIDE_L2PF
+#define SPROUT_WIDE_L2PF 4   // bulk L2 prefetch distance of the token planes, in iterations beyond the ring
+#endif
+
+__host__ __device__ inline size_t wide_team_bytes(int kcap, int kp) {
+    return (size_t)kWideCtl + (size_t)kWideStages * kWideStageBytes + (size_t)(kcap + 1) * 256 +
+           (size_t)kWideBuckets * 8 + (size_t)kp * 4;
+}
+
+struct WideSeg {       // the team's current segment (written by the consumer before the team barrier)
+    long long sl, s0, s1;
+    int meta, P;
+};
+
+struct WideSmem {
+    uint32_t bar_s;     // shared address of full[0] (full[i] = bar_s + 8i, empty[i] = bar_s + 8(S + i))
+    WideSeg *seg;
+    uint32_t ring_s;    // [S] stages of kWideStageBytes
+    uint2 *hist;        // [(kcap + 1) rows][32 lanes] packed rows
+    uint2 *lut;         // [kWideBuckets] {key, row offset}; after the stream: 64-bit rows [nb][4]
+    uint32_t *keys;     // [kp] sorted keys, padded with 0xFFFFFFFF
+    uint32_t hist_s, lut_s;
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t addr) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(addr), "r"(parity) : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t addr, uint32_t bytes) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(addr),
+                 "r"(bytes) : "memory");
+}
+// TMA bulk copy global -> shared (1D, 16-byte aligned, size a multiple of 16),
+// completing `bytes` of the transaction count of mbarrier `mbar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void team_sync(int team) {
+    asm volatile("bar.sync %0, 64;" ::"r"(team + 1) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+// Philox4x32-10 of the counter (lo, H, 0, 0), H the launch's constant high
+// word (reading L10: counter (g >> 2 lo32, g >> 2 hi32, 0, 0)).  Round 0's
+// second product is 0 and its first output word H ^ k0[0] = ph_a is
+// constant, so round 1's first product M0 * ph_a and round 2's c3 are launch
+// constants (host-computed ph_d, ph_e).  Bit-identical to philox4x32_10_rk.
+__device__ __forceinline__ Philox4 philox_lo(uint32_t lo, const SimArgs &a) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * lo;                // round 0
+    uint32_t c2 = (uint32_t)(p0 >> 32) ^ a.rk1[0];
+    uint32_t c3 = (uint32_t)p0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;               // round 1 (c0 = ph_a, c1 = 0)
+    uint32_t c0 = (uint32_t)(p1 >> 32) ^ a.rk0[1];
+    uint32_t c1 = (uint32_t)p1;
+    c2 = c3 ^ a.ph_d;
+    p0 = (uint64_t)0xD2511F53u * c0;                         // round 2 (c3 = lo32(M0 * ph_a))
+    p1 = (uint64_t)0xCD9E8D57u * c2;
+    c0 = (uint32_t)(p1 >> 32) ^ c1 ^ a.rk0[2];
+    c2 = (uint32_t)(p0 >> 32) ^ a.ph_e;
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+#pragma unroll
+    for (int r = 3; r < 10; ++r) {
+        p0 = (uint64_t)0xD2511F53u * c0;
+        p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ a.rk0[r];
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ a.rk1[r];
+        c1 = (uint32_t)p1;
+        c3 = (uint32_t)p0;
+        c0 = n0;
+        c2 = n2;
+    }
+    Philox4 o;
+    o.v[0] = c0; o.v[1] = c1; o.v[2] = c2; o.v[3] = c3;
+    return o;
+}
+
+struct WTok {
+    uint4 t[3];
+};
+
+// 32-bit word h (0..3) of a 128-bit group load (runtime h: select cascade)
+__device__ __forceinline__ uint32_t wword(const uint4 &u, int h) {
+    return h == 0 ? u.x : h == 1 ? u.y : h == 2 ? u.z : u.w;
+}
+// packed increments of request k of a group: word 0 = tok_0 + 1 << 20, word 1 = tok_1 | tok_2 << 16
+__device__ __forceinline__ uint2 wide_inc(const WTok &g, int k) {
+    const uint32_t w0 = wword(g.t[0], k >> 1), w1 = wword(g.t[1], k >> 1), w2 = wword(g.t[2], k >> 1);
+    return make_uint2(((k & 1) ? (w0 >> 16) : (w0 & 0xFFFFu)) + (1u << kW0Shift),
+                      __byte_perm(w1, w2, (k & 1) ? 0x7632u : 0x5410u));
+}
+
+// Bucket table over [0, 2^32) for the segment's K sorted keys: clear, scatter
+// the keys (count in .y, key in .x), then an exclusive prefix over the bucket
+// counts, 32 buckets per step.  Entry = {key, first bin * 256} for a bucket
+// with one key, {0xFFFFFFFF, first bin * 256} for none, {0xFFFFFFFF, 1} (odd:
+// the producer searches the keys) for two or more.
+__device__ __forceinline__ void wide_build_lut(const WideSmem &S, int K) {
+    const uint32_t lane = lane_id();
+    for (int b = (int)lane; b < kWideBuckets; b += 32) S.lut[b] = make_uint2(0xFFFFFFFFu, 0u);
+    __syncwarp();
+    for (int j = (int)lane; j < K; j += 32) {
+        const uint32_t key = S.keys[j];
+        const uint32_t b = key >> kWideShift;
+        atomicAdd(&S.lut[b].y, 1u);
+        atomicExch(&S.lut[b].x, key);   // meaningful only when the bucket holds exactly one key
+    }
+    __syncwarp();
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t run = 0u;
+#pragma unroll 4
+    for (int c = 0; c < kWideBuckets / 32; ++c) {
+        const int b = c * 32 + (int)lane;
+        const uint2 e = S.lut[b];
+        const uint32_t cnt = e.y;
+        uint32_t excl, total;
+        if (__any_sync(0xFFFFFFFFu, cnt >= 4u)) {
+            uint32_t x = cnt;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+                if ((int)lane >= d) x += y;
+            }
+            excl = x - cnt;
+            total = __shfl_sync(0xFFFFFFFFu, x, 31);
+        } else {
+            const uint32_t b0 = __ballot_sync(0xFFFFFFFFu, cnt & 1u), b1 = __ballot_sync(0xFFFFFFFFu, cnt & 2u);
+            excl = __popc(b0 & lt) + 2u * __popc(b1 & lt);
+            total = __popc(b0) + 2u * __popc(b1);
+        }
+        S.lut[b] = cnt >= 2u ? make_uint2(0xFFFFFFFFu, 1u)
+                             : make_uint2(cnt == 1u ? e.x : 0xFFFFFFFFu, (run + excl) * 256u);
+        run += total;
+    }
+    __syncwarp();
+}
+
+// 64-bit add of a packed row (or of one request's exact fields) into the spill scratch
+__device__ __forceinline__ void wide_spill_add(unsigned long long *scr, int bin, uint32_t cnt, uint32_t t0,
+                                               uint32_t t1, uint32_t t2) {
+    unsigned long long *r = scr + (size_t)bin * 4;
+    if (cnt) atomicAdd(&r[0], (unsigned long long)cnt);
+    if (t0) atomicAdd(&r[1], (unsigned long long)t0);
+    if (t1) atomicAdd(&r[2], (unsigned long long)t1);
+    if (t2) atomicAdd(&r[3], (unsigned long long)t2);
+}
+
+// the eight histogram rows (c0 = the consumer lane's slot) of a group's draws;
+// draws in buckets holding several keys take the exact bin by binary search
+__device__ __forceinline__ void wide_rows(const SimArgs &a, const WideSmem &S, const U8x &w, uint32_t c0,
+                                          uint32_t c1, int P, U8x &row) {
+    uint32_t odd = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint2 e = lds64(S.lut_s + ((w.v[k] >> kWideShift) << 3));
+        row.v[k] = e.y + (w.v[k] > e.x ? c1 : c0);
+        odd |= row.v[k];
+    }
+    if (odd & 1u) {   // rare: draws in multi-key buckets (odd row), exact bin by binary search
+        uint32_t m = 0u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m |= (row.v[k] & 1u) << k;
+#pragma unroll 1
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1u;
+            set8(row, k, c0 + (uint32_t)find_bin(S.keys, P, sel8(w, k)) * 256u);
+        }
+    }
+}
+
+// One ring stage: wait until it is free, start the TMA bulk copies of the
+// iteration's token planes (lane 0; the full barrier expects their bytes),
+// write the rows, then the second arrival on the full barrier.
+__device__ __forceinline__ void wide_put(const SimArgs &a, const WideSmem &S, const U8x &row, int64_t gi,
+                                         int64_t ge, uint32_t &cnt) {
+    const uint32_t lane = lane_id();
+    const uint32_t s = cnt % kWideStages, ph = (cnt / kWideStages) & 1u;
+    const uint32_t st = S.ring_s + s * (uint32_t)kWideStageBytes;
+    const uint32_t full = S.bar_s + 8u * s;
+    mbar_wait(S.bar_s + 8u * (kWideStages + s), ph ^ 1u);   // stage free
+    if (lane == 0) {
+        const int64_t ng = min((int64_t)32, ge - gi);        // whole groups of this iteration
+        const uint32_t bytes = (uint32_t)ng * 16u;
+        mbar_arrive_expect_tx(full, 3u * bytes);
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+            bulk_g2s(st + 1024u + 512u * q, a.tokens + (size_t)q * a.pitch + (size_t)gi * 8, bytes, full);
+        const int64_t gp = gi + 32 * (int64_t)(kWideStages + SPROUT_WIDE_L2PF);   // further ahead into L2
+        if (gp < ge) {
+            const uint32_t pb = (uint32_t)min((int64_t)32, ge - gp) * 16u;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) bulk_prefetch_l2(a.tokens + (size_t)q * a.pitch + (size_t)gp * 8, pb);
+        }
+    }
+    if (gi + (int64_t)lane < ge) {
+        sts128(st + lane * 16u, make_uint4(row.v[0], row.v[1], row.v[2], row.v[3]));
+        sts128(st + 512u + lane * 16u, make_uint4(row.v[4], row.v[5], row.v[6], row.v[7]));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(full);
+    ++cnt;
+}
+
+// Producer: per warp iteration i, lane l's group v = gf + l + 32i: its two
+// Philox calls, the eight rows (c0 = the consumer lane's slot), the exact
+// bin for draws in multi-key buckets, and the rows into ring stage cnt % S.
+// Two iterations at a time (four independent Philox chains in flight).
+__device__ __forceinline__ void wide_produce(const SimArgs &a, const WideSmem &S, int64_t gf, int64_t ge, int P,
+                                             uint32_t &cnt) {
+    const uint32_t lane = lane_id();
+    const uint32_t n_iter = ge > gf ? (uint32_t)((ge - gf + 31) >> 5) : 0u;
+    const uint32_t c0 = S.hist_s + lane * 8u, c1 = c0 + 256u;
+    const int64_t v0 = gf + lane;
+    uint32_t lo = (uint32_t)((a.first_request >> 2) + 2u * (uint64_t)v0);
+    if (lane < 3u * (kWideStages + SPROUT_WIDE_L2PF)) {   // the first iterations' planes into L2
+        const int64_t gp = gf + 32 * (int64_t)(lane / 3u);
+        if (gp < ge)
+            bulk_prefetch_l2(a.tokens + (size_t)(lane % 3u) * a.pitch + (size_t)gp * 8,
+                             (uint32_t)min((int64_t)32, ge - gp) * 16u);
+    }
+    uint32_t i = 0;
+#pragma unroll 1
+    for (; i + 2 <= n_iter; i += 2, lo += 128u) {
+        U8x w0, w1, r0, r1;
+#if SPROUT_WIDE_AB_NOPHILOX   // A/B timing only (wrong results): a cheap hash instead of Philox
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { w0.v[k] = (lo + k) * 0x9E3779B9u; w1.v[k] = (lo + 64u + k) * 0x9E3779B9u; }
+#else
+        const Philox4 d0 = philox_lo(lo, a), d1 = philox_lo(lo + 1u, a);
+        const Philox4 d2 = philox_lo(lo + 64u, a), d3 = philox_lo(lo + 65u, a);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            w0.v[k] = d0.v[k]; w0.v[4 + k] = d1.v[k];
+            w1.v[k] = d2.v[k]; w1.v[4 + k] = d3.v[k];
+        }
+#endif
+        wide_rows(a, S, w0, c0, c1, P, r0);
+        wide_rows(a, S, w1, c0, c1, P, r1);
+        wide_put(a, S, r0, gf + 32 * (int64_t)i, ge, cnt);
+        wide_put(a, S, r1, gf + 32 * (int64_t)(i + 1), ge, cnt);
+    }
+    if (i < n_iter) {
+        U8x w0, r0;
+        const Philox4 d0 = philox_lo(lo, a), d1 = philox_lo(lo + 1u, a);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) { w0.v[k] = d0.v[k]; w0.v[4 + k] = d1.v[k]; }
+        wide_rows(a, S, w0, c0, c1, P, r0);
+        wide_put(a, S, r0, gf + 32 * (int64_t)i, ge, cnt);
+    }
+}
+
+// Consumer rare work of a group (inline, rolled): big -- some token >= 4096,
+// so a 16-bit field may have wrapped: the group's eight increments are
+// reverted (exact: 32-bit word arithmetic is modular) and its requests added
+// exactly into the 64-bit scratch; then rows with a guard bit set spill.
+__device__ __forceinline__ void wide_rare(const WTok &g, const U8x &rows, uint32_t big, uint32_t c0,
+                                          unsigned long long *scr, uint32_t &spilled) {
+    if (big) {
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t r = sel8(rows, k);
+            const uint2 inc = wide_inc(g, k);
+            uint2 A = lds64(r);
+            A.x -= inc.x;
+            A.y -= inc.y;
+            sts64(r, A);
+        }
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t w0 = wword(g.t[0], k >> 1), w1 = wword(g.t[1], k >> 1), w2 = wword(g.t[2], k >> 1);
+            const int sh = (k & 1) * 16;
+            wide_spill_add(scr, (int)((sel8(rows, k) - c0) >> 8), 1u, (w0 >> sh) & 0xFFFFu, (w1 >> sh) & 0xFFFFu,
+                           (w2 >> sh) & 0xFFFFu);
+        }
+        spilled = 1u;
+        return;
+    }
+#pragma unroll 1
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t r = sel8(rows, k);
+        const uint2 A = lds64(r);
+        if ((A.x & kGuard0) | (A.y & kGuard)) {
+            wide_spill_add(scr, (int)((r - c0) >> 8), A.x >> kW0Shift, A.x & kW0Low, A.y & 0xFFFFu, A.y >> 16);
+            sts64(r, make_uint2(0u, 0u));
+            spilled = 1u;
+        }
+    }
+}
+
+// Consumer: lane l's groups gf + l + 32i; per iteration it waits for the
+// stage (rows written, token planes landed), reads its eight rows and its
+// three 16-byte token words, releases the stage, then does the serial
+// read-modify-writes and one test for the rare work.
+__device__ __forceinline__ void wide_consume(const SimArgs &a, const WideSmem &S, int64_t gf, int64_t ge,
+                                             unsigned long long *scr, uint32_t &spilled, uint32_t &cnt) {
+    const uint32_t lane = lane_id();
+    const uint32_t n_iter = ge > gf ? (uint32_t)((ge - gf + 31) >> 5) : 0u;
+    const int64_t v0 = gf + lane;
+    const uint32_t n_mine = v0 < ge ? (uint32_t)((ge - v0 + 31) >> 5) : 0u;
+    const uint32_t c0 = S.hist_s + lane * 8u;
+#pragma unroll 1
+    for (uint32_t i = 0; i < n_iter; ++i) {
+        const uint32_t s = cnt % kWideStages, ph = (cnt / kWideStages) & 1u;
+        const uint32_t st = S.ring_s + s * (uint32_t)kWideStageBytes + lane * 16u;
+        mbar_wait(S.bar_s + 8u * s, ph);   // rows written and token planes landed
+        U8x row;
+        WTok g;
+        {
+            const uint4 r0 = lds128(st), r1 = lds128(st + 512u);
+            row.v[0] = r0.x; row.v[1] = r0.y; row.v[2] = r0.z; row.v[3] = r0.w;
+            row.v[4] = r1.x; row.v[5] = r1.y; row.v[6] = r1.z; row.v[7] = r1.w;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) g.t[q] = lds128(st + 1024u + 512u * q);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(S.bar_s + 8u * (kWideStages + s));   // stage free again
+        ++cnt;
+        if (i < n_mine) {
+            uint32_t acc0 = 0u, acc1 = 0u;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint2 inc = wide_inc(g, k);
+                uint2 A = lds64(row.v[k]);
+                A.x += inc.x;
+                A.y += inc.y;
+                sts64(row.v[k], A);
+                acc0 |= A.x;
+                acc1 |= A.y;
+            }
+            const uint32_t big = (g.t[0].x | g.t[0].y | g.t[0].z | g.t[0].w | g.t[1].x | g.t[1].y | g.t[1].z |
+                                  g.t[1].w | g.t[2].x | g.t[2].y | g.t[2].z | g.t[2].w) & kBigTok;
+            if ((acc0 & kGuard0) | (acc1 & kGuard) | big) wide_rare(g, row, big, c0, scr, spilled);
+        }
+    }
+}
+
+// the requests outside the segment's whole groups (at most 7 at each end),
+// one per lane, added exactly into the spill scratch
+__device__ __forceinline__ void wide_ends(const SimArgs &a, const WideSmem &S, int64_t s0, int64_t s1, int P,
+                                          unsigned long long *scr, uint32_t &spilled) {
+    const uint32_t lane = lane_id();
+    const int64_t h_end = min(s1, (s0 + 7) & ~(int64_t)7);
+    const int64_t t_beg = max(h_end, s1 & ~(int64_t)7);
+    int64_t r = -1;
+    if ((int64_t)lane < h_end - s0) r = s0 + lane;
+    else if (lane >= 8 && (int64_t)(lane - 8) < s1 - t_beg) r = t_beg + (lane - 8);
+    if (r < 0) return;
+    const uint64_t gidx = a.first_request + (uint64_t)r;
+    const Philox4 d = philox_lo((uint32_t)(gidx >> 2), a);
+    const uint32_t k3 = (uint32_t)(gidx & 3u);
+    const uint32_t w = k3 == 0 ? d.v[0] : k3 == 1 ? d.v[1] : k3 == 2 ? d.v[2] : d.v[3];
+    wide_spill_add(scr, find_bin(S.keys, P, w), 1u, a.tokens[r], a.tokens[(size_t)a.pitch + r],
+                   a.tokens[2 * (size_t)a.pitch + r]);
+    spilled = 1u;
+}
+
+// lane histograms (+ the spill scratch) -> 64-bit rows 0..K of the table
+// space, rows K+1 and the pinned row cleared, then the exclusive prefix over
+// bins 0..K+1 per field (the layout cell_epilogue / write_seg_stats read)
+__device__ __forceinline__ void wide_readout(const SimArgs &a, const WideSmem &S, int K, bool spilled,
+                                             unsigned long long *scr) {
+    const uint32_t lane = lane_id();
+    unsigned long long *wide = reinterpret_cast<unsigned long long *>(S.lut);
+    for (int bn = (int)lane; bn <= K; bn += 32) {
+        uint2 *row = S.hist + (size_t)bn * 32;
+        uint32_t sv[4] = {0u, 0u, 0u, 0u};
+#pragma unroll 8
+        for (int q = 0; q < 32; ++q) {
+            const int idx = (q + (int)lane) & 31;   // rotated: conflict-free
+            const uint2 val = row[idx];
+            row[idx] = make_uint2(0u, 0u);
+            sv[0] += val.x >> kW0Shift;
+            sv[1] += val.x & kW0Low;
+            sv[2] += val.y & 0xFFFFu;
+            sv[3] += val.y >> 16;
+        }
+        unsigned long long f[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f[j] = sv[j];
+        if (spilled) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                f[j] += scr[(size_t)bn * 4 + j];
+                scr[(size_t)bn * 4 + j] = 0ull;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) wide[(size_t)bn * 4 + j] = f[j];
+    }
+    if (lane < 4) {
+        wide[(size_t)(K + 1) * 4 + lane] = 0ull;
+        wide[(size_t)(a.nb - 1) * 4 + lane] = 0ull;
+    }
+    __syncwarp();
+    if (lane < 4) {
+        unsigned long long run = 0ull;
+        for (int bn = 0; bn <= K + 1; ++bn) {
+            unsigned long long *pt = &wide[(size_t)bn * 4 + lane];
+            const unsigned long long v2 = *pt;
+            *pt = run;
+            run += v2;
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(64 * kWideTeams, 1) trace_wide_kernel(const __grid_constant__ SimArgs a) {
+    constexpr int N = 3;
+    constexpr int kExit = -9;
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ CostConst cost;
+    const int warp = threadIdx.x >> 5;
+    const int team = warp >> 1;
+    const bool producer = (warp & 1) != 0;
+    const uint32_t lane = lane_id();
+    const int X = a.X, nb = a.nb, kcap = a.kcap;
+    WideSmem S;
+    {
+        uint8_t *base = smem + (size_t)team * a.warp_smem;
+        S.bar_s = smem_u32(base);
+        S.seg = reinterpret_cast<WideSeg *>(base + 16 * kWideStages);
+        S.ring_s = smem_u32(base + kWideCtl);
+        uint8_t *h = base + kWideCtl + (size_t)kWideStages * kWideStageBytes;
+        S.hist = reinterpret_cast<uint2 *>(h);
+        S.lut = reinterpret_cast<uint2 *>(h + (size_t)(kcap + 1) * 256);
+        S.keys = reinterpret_cast<uint32_t *>(h + (size_t)(kcap + 1) * 256 + (size_t)kWideBuckets * 8);
+        S.hist_s = smem_u32(S.hist);
+        S.lut_s = smem_u32(S.lut);
+    }
+    for (int i = threadIdx.x; i < (int)(sizeof(CostConst) / 8); i += blockDim.x)
+        reinterpret_cast<double *>(&cost)[i] = reinterpret_cast<const double *>(&a.cost)[i];
+    if (!producer) {
+        for (int i = lane; i < (kcap + 1) * 32; i += 32) S.hist[i] = make_uint2(0u, 0u);
+        if (lane < 2 * kWideStages) mbar_init(S.bar_s + 8u * lane, lane < kWideStages ? 2u : 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");   // visible to the TMA unit
+    }
+    __syncthreads();
+    uint32_t cnt = 0u;   // ring iterations so far (both warps of a team count the same)
+
+    if (producer) {
+        for (;;) {
+            team_sync(team);
+            const WideSeg sg = *S.seg;
+            if (sg.meta == kExit) break;
+            if (sg.meta >= 1) wide_produce(a, S, (sg.s0 + 7) >> 3, sg.s1 >> 3, sg.P, cnt);
+        }
+        return;
+    }
+
+    // consumer
+    WarpSmem W;   // the view the shared epilogue and the K = 0 / slow paths use
+    W.hist = S.hist;
+    W.wide = reinterpret_cast<unsigned long long *>(S.lut);
+    W.lut = S.lut;
+    W.keys = S.keys;
+    unsigned long long *scr = a.wide_scratch + ((size_t)blockIdx.x * kWideTeams + team) * (size_t)(kcap + 1) * 4;
+    for (int i = lane; i < (kcap + 1) * 4; i += 32) scr[i] = 0ull;
+    uint32_t err = 0u;
+    constexpr int kKeyRegs = 4;   // keys prefetched per lane (kcap <= 128), else read at use
+    struct SegPre {
+        int64_t sl, s0, s1;
+        int meta;
+        double k0;
+        uint32_t key[kKeyRegs];
+        SegCells sc;
+    };
+    const bool pre_cells = X <= 64;
+    auto load_pre = [&](int64_t sl) {
+        SegPre p;
+        p.sl = sl;
+        p.meta = -3;
+        p.s0 = p.s1 = 0;
+        p.k0 = 0.0;
+#pragma unroll
+        for (int t = 0; t < kKeyRegs; ++t) p.key[t] = 0xFFFFFFFFu;
+        p.sc.st[0] = p.sc.st[1] = 0xFFu;
+        p.sc.bw[0] = p.sc.bw[1] = 0u;
+        if (sl < a.n_segments) {
+            p.meta = a.seg_meta[sl];
+            p.s0 = a.seg_offsets[sl];
+            p.s1 = a.seg_offsets[sl + 1];
+            p.k0 = a.k0[a.first_segment + sl];
+            if (pre_cells) {
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    const int j = (int)lane + 32 * t;
+                    if (j < X) {
+                        const int64_t cell = sl * X + j;
+                        p.sc.st[t] = a.cell_status[cell];
+                        p.sc.bw[t] = *reinterpret_cast<const uint32_t *>(a.seg_bnd + cell * 2);
+                    }
+                }
+            }
+            if (kcap <= 32 * kKeyRegs) {
+#pragma unroll
+                for (int t = 0; t < kKeyRegs; ++t) {
+                    const int i = (int)lane + 32 * t;
+                    if (i < kcap) p.key[t] = a.seg_keys[sl * kcap + i];
+                }
+            }
+        }
+        return p;
+    };
+    const int64_t B = a.seg_batch;
+    int64_t it_seg = 0, it_end = 0;
+    uint32_t pend = 0u;
+    if (lane == 0) pend = atomicAdd(a.queue, 1u);
+    auto next_segment = [&]() -> int64_t {
+        if (it_seg >= it_end) {
+            it_seg = (int64_t)__shfl_sync(0xFFFFFFFFu, pend, 0) * B;
+            it_end = min(it_seg + B, a.n_segments);
+            if (it_seg >= a.n_segments) return a.n_segments;
+            if (lane == 0) pend = atomicAdd(a.queue, 1u);
+        }
+        return it_seg++;
+    };
+    auto zero_wide = [&](int rows) {   // 64-bit rows 0..rows-1 and the pinned row
+        for (int i = lane; i < rows * (N + 1); i += 32) W.wide[i] = 0ull;
+        if (lane < N + 1) W.wide[(size_t)(nb - 1) * (N + 1) + lane] = 0ull;
+        __syncwarp();
+    };
+    SegPre cur = load_pre(next_segment());
+    for (;;) {
+        const int64_t sl = cur.sl;
+        if (sl >= a.n_segments) {
+            if (lane == 0) S.seg->meta = kExit;
+            team_sync(team);
+            break;
+        }
+        const SegPre nxt = load_pre(next_segment());
+        const int64_t s = a.first_segment + sl;
+        const int meta = cur.meta;
+        const double *qrow =
+            a.q + (a.profile_per_interval ? s : (s < 0xFFFFFFFFll ? (int64_t)a.div_t.div((uint32_t)s) : s / a.T)) * N;
+        const double kp = cur.k0 * a.pue;
+        const int64_t s0 = cur.s0, s1 = cur.s1;
+        const int K = meta;
+        int P = 1;
+        while (P < K + 1) P <<= 1;
+        if (meta >= 0) {
+            if (kcap <= 32 * kKeyRegs) {
+#pragma unroll
+                for (int t = 0; t < kKeyRegs; ++t) {
+                    const int i = (int)lane + 32 * t;
+                    if (i < P) S.keys[i] = i < K ? cur.key[t] : 0xFFFFFFFFu;
+                }
+            } else {
+                for (int i = lane; i < P; i += 32) S.keys[i] = i < K ? a.seg_keys[sl * kcap + i] : 0xFFFFFFFFu;
+            }
+            __syncwarp();
+            if (K >= 1) wide_build_lut(S, K);
+        }
+        if (lane == 0) {
+            S.seg->sl = sl; S.seg->s0 = s0; S.seg->s1 = s1;
+            S.seg->meta = meta; S.seg->P = P;
+        }
+        team_sync(team);   // the producer may start on this segment
+        if (meta == -2) {   // invalid offsets: segment skipped, outputs zero
+            err |= SPROUT_TRACE_BAD_OFFSETS;
+            for (int j = lane; j < X; j += 32) zero_cell(a, sl * X + j, N);
+            if (lane == 0) { a.seg_count[sl] = 0ull; a.seg_pinned[sl] = 0ull; }
+            if (lane < N) a.seg_tok[sl * N + lane] = 0ull;
+            if (lane < 4) a.seg_base[sl * 4 + lane] = 0.0;
+            cur = nxt;
+            continue;
+        }
+        if (meta == -1) {
+            zero_wide(2);
+            slow_segment<N, false>(a, W, sl, s0, s1, err);
+            cell_epilogue<N>(a, W, sl, 0, kp, qrow, false, cost, false, cur.sc);
+            __syncwarp();
+            write_seg_stats<N>(a, W, sl, kp, qrow[0], 0, 1, false, cost);
+            __syncwarp();
+            cur = nxt;
+            continue;
+        }
+        if (K == 0) {
+            zero_wide(2);
+            stream_segment_k0<N>(a, W, s0, s1);
+            __syncwarp();
+            if (lane < N + 1) {   // exclusive prefix over bins 0..1
+                const unsigned long long v0 = W.wide[lane];
+                W.wide[lane] = 0ull;
+                W.wide[(N + 1) + lane] = v0;
+            }
+            __syncwarp();
+        } else {
+            uint32_t spilled = 0u;
+            wide_ends(a, S, s0, s1, P, scr, spilled);
+            wide_consume(a, S, (s0 + 7) >> 3, s1 >> 3, scr, spilled, cnt);
+            __syncwarp();
+            __threadfence_block();
+            const bool any_spill = __any_sync(0xFFFFFFFFu, spilled != 0u);
+            wide_readout(a, S, K, any_spill, scr);
+        }
+        // the next segment's first groups into L2 while this one's epilogue runs
+        if (nxt.sl < a.n_segments && nxt.meta >= -1 && nxt.s1 > nxt.s0) {
+            const int64_t g0 = nxt.s0 >> 3, g1 = (nxt.s1 - 1) >> 3;
+            if (nxt.s1 - nxt.s0 < 2048) {
+                const int64_t v = (lane < 16) ? g0 + lane : g1 - (int64_t)(lane - 16);
+                if (v >= g0 && v <= g1) {
+#pragma unroll
+                    for (int i = 0; i < N; ++i)
+                        prefetch_l2(reinterpret_cast<const uint4 *>(a.tokens + (size_t)i * a.pitch) + v);
+                }
+            } else {
+#pragma unroll 1
+                for (int it = 0; it <= SPROUT_WIDE_PREFETCH; ++it) {
+                    const int64_t v = it < SPROUT_WIDE_PREFETCH ? g0 + lane + 32 * it : g1;
+#pragma unroll
+                    for (int i = 0; i < N; ++i)
+                        prefetch_l2(reinterpret_cast<const uint4 *>(a.tokens + (size_t)i * a.pitch) + v);
+                }
+            }
+        }
+        cell_epilogue<N>(a, W, sl, K, kp, qrow, true, cost, pre_cells, cur.sc);
+        __syncwarp();
+        write_seg_stats<N>(a, W, sl, kp, qrow[0], K + 1, nb - 1, true, cost);
+        __syncwarp();
+        cur = nxt;
+    }
+    err = __reduce_or_sync(0xFFFFFFFFu, err);
+    if (lane == 0 && err) atomicOr(a.trace_status, err);
+}
+
+// ---------------------------------------------------------------------------
 // verify mode (levels_out): the level of every request in every cell of its
 // segment, from the same draw, the same breakpoint keys and the same
 // per-cell bin boundaries the streaming kernel aggregates over (or, for
@@ -1585,6 +2290,13 @@ bool make_sim_plan(int n, int X, int NC, SimPlan *plan, int max_keys) {
     return true;
 }
 
+// spill scratch of trace_wide_kernel (n = 3): [kWideMaxSMs * kWideTeams][kcap + 1][4] u64
+static size_t wide_scratch_bytes(const SimPlan &p) {
+    if (!SPROUT_ENABLE_WIDE || p.n != 3) return 0;
+    const int kc = nominal_kcap(p.n, p.X);
+    return ((size_t)kWideMaxSMs * kWideTeams * (size_t)(kc + 1) * 4 * 8 + 255) & ~(size_t)255;
+}
+
 size_t sim_workspace_bytes(const SimPlan &p, int64_t n_segments) {
     const int kc = nominal_kcap(p.n, p.X);
     size_t b = 256;                                             // queue
@@ -1592,7 +2304,40 @@ size_t sim_workspace_bytes(const SimPlan &p, int64_t n_segments) {
     b += ((size_t)n_segments * kc * 4 + 255) & ~(size_t)255;   // seg_keys
     const size_t cells = (size_t)n_segments * p.X;
     b += (cells * (p.n > 1 ? p.n - 1 : 0) * 2 + 255) & ~(size_t)255;  // seg_bnd
+    b += wide_scratch_bytes(p);
     return b;
+}
+
+// trace_wide_kernel applies: n = 3, one class, no flags plane, X > 1, a
+// breakpoint bound that fits its table space, and a launch whose Philox
+// blocks share one high counter word
+static bool wide_applies(const SimArgs &a, const SimPlan &plan) {
+    if (!SPROUT_ENABLE_WIDE || plan.n != 3 || a.flags || a.NC != 1 || a.X <= 1) return false;
+    if (plan.kcap < 1 || plan.kcap > kWideMaxKeys) return false;
+    if (a.n_requests > 0 && (a.first_request >> 34) != ((a.first_request + (uint64_t)a.n_requests - 1) >> 34))
+        return false;
+    int kp = 1;
+    while (kp < plan.kcap + 1) kp <<= 1;
+    return (size_t)kWideTeams * ((wide_team_bytes(plan.kcap, kp) + 15) & ~(size_t)15) <= (227 * 1024 - 2048);
+}
+
+static cudaError_t launch_trace_wide(SimArgs &a, const SimPlan &plan, cudaStream_t stream) {
+    int kp = 1;
+    while (kp < plan.kcap + 1) kp <<= 1;
+    a.warp_smem = (wide_team_bytes(plan.kcap, kp) + 15) & ~(size_t)15;   // per team
+    if ((size_t)kWideTeams * a.warp_smem > 227 * 1024 - 2048) return cudaErrorInvalidConfiguration;
+    const int threads = kWideTeams * 64;
+    const size_t smem = a.warp_smem * kWideTeams;
+    cudaError_t e = cudaFuncSetAttribute(trace_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t grid = sms < kWideMaxSMs ? sms : kWideMaxSMs;   // one CTA per SM (the spill scratch covers them)
+    const int64_t need = (a.n_segments + kWideTeams - 1) / kWideTeams;
+    if (grid > need) grid = need > 0 ? need : 1;
+    trace_wide_kernel<<<(unsigned)grid, threads, smem, stream>>>(a);
+    return cudaGetLastError();
 }
 
 template <int N, bool FLAGS>
@@ -1618,6 +2363,7 @@ static cudaError_t launch_trace_t(SimArgs &a, const SimPlan &plan, cudaStream_t 
 template <int N>
 static cudaError_t launch_n(SimArgs &a, const SimPlan &plan, cudaStream_t stream, int *launches) {
     cudaError_t e = (!kDisableX1 && trace_x1_supported(N, a.X, a.NC)) ? launch_trace_x1(a, stream)
+                  : (N == 3 && a.wide) ? launch_trace_wide(a, plan, stream)
                   : a.flags ? launch_trace_t<N, true>(a, plan, stream) : launch_trace_t<N, false>(a, plan, stream);
     if (e != cudaSuccess) return e;
     ++*launches;
@@ -1642,6 +2388,8 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
     const int kc = nominal_kcap(plan.n, plan.X);
     off += ((size_t)a.n_segments * kc * 4 + 255) & ~(size_t)255;
     a.seg_bnd = reinterpret_cast<uint16_t *>(w + off);
+    off += ((size_t)a.n_segments * plan.X * (plan.n > 1 ? plan.n - 1 : 0) * 2 + 255) & ~(size_t)255;
+    a.wide_scratch = reinterpret_cast<unsigned long long *>(w + off);
     a.kcap = plan.kcap;   // -1 (all slow) or the plan's bound <= kc (the seg_keys stride)
     a.nb = plan.nb;
     a.nw = plan.nw;
@@ -1666,7 +2414,15 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
             a.rk0[r] = k0; a.rk1[r] = k1;
             k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
         }
+        // philox_lo's launch constants for the counter high word H of the launch's blocks
+        const uint32_t H = (uint32_t)(a.first_request >> 34);
+        a.ph_a = H ^ a.rk0[0];
+        const uint64_t B = (uint64_t)0xD2511F53u * a.ph_a;
+        a.ph_blo = (uint32_t)B;
+        a.ph_d = (uint32_t)(B >> 32) ^ a.rk1[1];
+        a.ph_e = (uint32_t)B ^ a.rk1[2];
     }
+    a.wide = wide_applies(a, plan) ? 1 : 0;
 
     // prep (also resets the queue and trace_status)
     {

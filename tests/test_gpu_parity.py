@@ -193,6 +193,41 @@ def test_count_spill_single_bin():
     check_full(w, levels=False)
 
 
+def test_wide_kernel_spills_long_segment():
+    # n = 3, one class, no flags, X > 1: trace_wide_kernel.  One 2M-request
+    # segment with two bins (xi = 0 is pure L0, xi = 1 has one breakpoint):
+    # every lane's rows pass their guard bits many times (64-bit spill scratch)
+    w = _custom(N=2_000_000, T=1, R=1, xi=[0.0, 1.0])
+    got, _ = check_full(w, levels=False)
+    assert (got["trace_status"] & S.TRACE_SLOW_PATH) == 0
+
+
+def test_wide_kernel_crowded_keys_and_bad_offsets():
+    # many xi values with nearly equal mixes put several keys in one bucket
+    # (the trap row and its repair), ragged/empty segments, head and tail
+    # requests outside whole groups; then non-monotone offsets are skipped
+    w = _custom(N=400_000, T=9, R=2, X=96, xi=np.concatenate([np.linspace(0.0, 1.0, 48),
+                                                            np.linspace(0.40, 0.4001, 48)]))
+    off = w.spec.seg_offsets
+    m = np.diff(off)
+    m[3] = 0
+    m[4] = 13
+    m[5] += 7
+    off[1:] = np.cumsum(m)
+    check_full(w, levels=True)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, flags = synth.host_trace(w.spec, sh)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=flags)
+    sw.solve()
+    bad = sw.trace.seg_offsets.clone(); bad[6] = bad[7] + 1
+    sw.trace.seg_offsets = bad
+    sw.simulate()
+    torch.cuda.synchronize()
+    got = sw.host()
+    assert got["trace_status"] & S.TRACE_BAD_OFFSETS
+    assert not got["cnt"].reshape(-1, w.prob.X, 3)[6].any()
+
+
 def test_arbitrary_thresholds_slow_path():
     # user-supplied thresholds with more distinct breakpoints than the fast
     # path holds (kcap = X+1): the generic per-cell path, still exact

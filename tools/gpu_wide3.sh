@@ -1,0 +1,7 @@
+#!/bin/bash
+TAG=${1:-w}; VARS=${2:-new old}
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "wide or c4 or levels_classes or empty or large_tokens" > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_$TAG.log
+bash tools/gpu_exp.sh $TAG "$VARS" C4 1
+export SPROUT_LIB_NAME=libsprout_new.so
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"trace_(wide_)?kernel" -s 2 -c 1 -o gpurun_out/prof_${TAG}_new python bench.py --config C4 --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_${TAG}.log 2>&1; echo "ncu rc=$?"
