@@ -360,23 +360,27 @@ sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *problem, do
  * window.  Writes every field of `solution` and every field of `totals`
  * (cells: cnt, tok, energy_kwh, time_s, carbon_g, quality; segments:
  * seg_count, seg_pinned, seg_tok, seg_base -- the same values
- * sprout_simulate_trace gives, they do not depend on the scheme; and
- * trace_status), so sprout_reduce_totals can follow directly.  Invalid
- * offsets (s0 > s1, or past n_requests) flag SPROUT_TRACE_BAD_OFFSETS and
- * the interval is skipped: its cells and segment fields are zero and no
- * request enters a window.  `profile_out` is NULL or (device)
- * [cells][2][n]: the e and p each interval's LP used.  One CTA per group of
- * up to 4 xi chains of a region (they share the requests' draws, tokens and
- * flags); sequential in t by definition.  Requires whole regions
+ * sprout_simulate_trace gives for the solved thresholds; and trace_status),
+ * so sprout_reduce_totals can follow directly.  Invalid offsets (s0 > s1,
+ * or past n_requests) flag SPROUT_TRACE_BAD_OFFSETS and the interval is
+ * skipped: its cells and segment fields are zero and no request enters a
+ * window.  `profile_out` is NULL or (device) [cells][2][n]: the e and p each
+ * interval's LP used.  Two passes: one CTA per (region, xi) chain solves the
+ * chain's LPs in interval order and, per interval, scans its requests
+ * backwards from the interval end only until every level the mix can reach
+ * has its last `window` requests (the windows need no more); then the
+ * streaming kernel of sprout_simulate_trace accounts every request with the
+ * solved thresholds.  `workspace` (device, 256-byte aligned, caller-owned,
+ * >= sprout_workspace_bytes) is that pass's.  Requires whole regions
  * (first_segment and n_segments multiples of n_intervals: a rank may take a
  * range of regions; outputs are indexed by local cell), profile_per_interval
- * 0, and 1 <= window <= 4096 with n*window*4 bytes <= 192 KiB.  Errors:
+ * 0, and 1 <= window <= 4096 with n*window*4 bytes <= 96 KiB.  Errors:
  * INVALID_ARGUMENT (as sprout_simulate_trace, plus the above); CUDA. */
 sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int32_t window,
                                           const sprout_trace *trace, const sprout_cost_model *cost,
                                           const sprout_lp_solution *solution,
                                           const sprout_cell_totals *totals, double *profile_out,
-                                          sprout_stream stream);
+                                          void *workspace, size_t workspace_bytes, sprout_stream stream);
 
 /* ---------------------------------------------------------------------- */
 /* NEXT-4: per-request outputs, the latent best level and the
@@ -476,7 +480,8 @@ sprout_status sprout_evaluation_q(const sprout_evaluator_problem *ev, const spro
 sprout_status sprout_simulate_closed_loop_q(const sprout_lp_problem *problem, int32_t window, const double *q_interval,
                                             const sprout_trace *trace, const sprout_cost_model *cost,
                                             const sprout_lp_solution *solution, const sprout_cell_totals *totals,
-                                            double *profile_out, sprout_stream stream);
+                                            double *profile_out, void *workspace, size_t workspace_bytes,
+                                            sprout_stream stream);
 
 /* Number of kernel launches (not memsets) the last successful call of each
  * entry point on this thread enqueued -- for launch accounting in benches. */

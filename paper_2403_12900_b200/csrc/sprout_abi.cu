@@ -203,17 +203,26 @@ sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *P, double *
     return st;
 }
 
+static sprout_status simulate_impl(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                   const sprout_trace *trace, const sprout_cost_model *cost,
+                                   const sprout_cell_totals *totals, uint8_t *levels_out, int32_t max_breakpoints,
+                                   void *workspace, size_t workspace_bytes, sprout_stream stream,
+                                   const double *q_rows);
+
 sprout_status sprout_simulate_closed_loop(const sprout_lp_problem *problem, int32_t window,
                                           const sprout_trace *trace, const sprout_cost_model *cost,
                                           const sprout_lp_solution *solution, const sprout_cell_totals *totals,
-                                          double *profile_out, sprout_stream stream) {
-    return sprout_simulate_closed_loop_q(problem, window, nullptr, trace, cost, solution, totals, profile_out, stream);
+                                          double *profile_out, void *workspace, size_t workspace_bytes,
+                                          sprout_stream stream) {
+    return sprout_simulate_closed_loop_q(problem, window, nullptr, trace, cost, solution, totals, profile_out,
+                                         workspace, workspace_bytes, stream);
 }
 
 sprout_status sprout_simulate_closed_loop_q(const sprout_lp_problem *problem, int32_t window, const double *q_interval,
                                             const sprout_trace *trace, const sprout_cost_model *cost,
                                             const sprout_lp_solution *solution, const sprout_cell_totals *totals,
-                                            double *profile_out, sprout_stream stream) {
+                                            double *profile_out, void *workspace, size_t workspace_bytes,
+                                            sprout_stream stream) {
     if (q_interval && !aligned(q_interval, 8)) return SPROUT_ERR_INVALID_ARGUMENT;
     sprout_status st = validate_problem(problem);
     if (st == SPROUT_OK) st = validate_solution(problem, solution);
@@ -227,8 +236,14 @@ sprout_status sprout_simulate_closed_loop_q(const sprout_lp_problem *problem, in
         problem->profile_per_interval != 0)
         return SPROUT_ERR_INVALID_ARGUMENT;
     const int64_t S = problem->n_segments;
-    if (window < 1 || window > 4096 || (int64_t)problem->n_levels * window * 4 > 192 * 1024)
+    if (window < 1 || window > 4096 || (int64_t)problem->n_levels * window * 4 > 96 * 1024)
         return SPROUT_ERR_INVALID_ARGUMENT;
+    {   // the totals pass's workspace (sprout_workspace_bytes)
+        SimPlan plan;
+        if (!make_sim_plan(problem->n_levels, problem->n_xi, cost->n_classes, &plan) || !workspace ||
+            workspace_bytes < sim_workspace_bytes(plan, problem->n_segments) || !aligned(workspace, 256))
+            return SPROUT_ERR_INVALID_ARGUMENT;
+    }
     if (profile_out && !aligned(profile_out, 8)) return SPROUT_ERR_INVALID_ARGUMENT;
     ClosedArgs a{};
     a.n = problem->n_levels; a.R = problem->n_regions; a.X = problem->n_xi; a.NC = cost->n_classes; a.W = window;
@@ -258,10 +273,14 @@ sprout_status sprout_simulate_closed_loop_q(const sprout_lp_problem *problem, in
     a.seg_count = totals->seg_count; a.seg_pinned = totals->seg_pinned; a.seg_tok = totals->seg_tok;
     a.seg_base = totals->seg_base;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (cudaMemsetAsync(totals->trace_status, 0, 4, s) != cudaSuccess) return SPROUT_ERR_CUDA;
     int launches = 0;
-    st = cuda_status(launch_closed_loop(a, s, &launches));
-    if (st == SPROUT_OK) g_last_launches = launches;
+    st = cuda_status(launch_closed_loop(a, s, &launches));   // every interval's LP, the windows
+    if (st != SPROUT_OK) return st;
+    // the totals of the solved thresholds: the open-loop streaming pass (cells,
+    // segments, trace_status), quality rows per interval when q varies
+    st = simulate_impl(problem, solution, trace, cost, totals, nullptr, 0, workspace, workspace_bytes, stream,
+                       q_interval);
+    if (st == SPROUT_OK) g_last_launches += launches;
     return st;
 }
 
@@ -282,11 +301,13 @@ sprout_status sprout_simulate_trace(const sprout_lp_problem *problem, const spro
                                          workspace_bytes, stream);
 }
 
-sprout_status sprout_simulate_trace_bounded(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
-                                            const sprout_trace *trace, const sprout_cost_model *cost,
-                                            const sprout_cell_totals *totals, uint8_t *levels_out,
-                                            int32_t max_breakpoints, void *workspace, size_t workspace_bytes,
-                                            sprout_stream stream) {
+// the streaming simulate (steps a5-a8) of a solution; q_rows (NULL: the
+// problem's q) overrides the quality rows with one per interval
+static sprout_status simulate_impl(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                   const sprout_trace *trace, const sprout_cost_model *cost,
+                                   const sprout_cell_totals *totals, uint8_t *levels_out, int32_t max_breakpoints,
+                                   void *workspace, size_t workspace_bytes, sprout_stream stream,
+                                   const double *q_rows) {
     if (max_breakpoints < 0) return SPROUT_ERR_INVALID_ARGUMENT;
     sprout_status st = validate_problem(problem);
     if (st == SPROUT_OK) st = validate_solution(problem, solution);
@@ -305,6 +326,7 @@ sprout_status sprout_simulate_trace_bounded(const sprout_lp_problem *problem, co
     a.T = problem->n_intervals; a.first_segment = problem->first_segment; a.n_segments = problem->n_segments;
     a.profile_per_interval = problem->profile_per_interval;
     a.k0 = problem->k0; a.q = problem->q; a.k1 = problem->k1; a.pue = problem->pue;
+    if (q_rows) { a.q = q_rows; a.profile_per_interval = 1; }
     a.threshold = solution->threshold; a.max_level = solution->max_level; a.cell_status = solution->cell_status;
     a.n_requests = trace->n_requests; a.first_request = trace->first_request; a.seg_offsets = trace->seg_offsets;
     a.tokens = trace->tokens; a.pitch = trace->plane_pitch; a.flags = trace->flags; a.seed = cost->seed;
@@ -321,6 +343,15 @@ sprout_status sprout_simulate_trace_bounded(const sprout_lp_problem *problem, co
     st = cuda_status(launch_simulate(a, plan, workspace, reinterpret_cast<cudaStream_t>(stream), &launches));
     if (st == SPROUT_OK) g_last_launches = launches;
     return st;
+}
+
+sprout_status sprout_simulate_trace_bounded(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                            const sprout_trace *trace, const sprout_cost_model *cost,
+                                            const sprout_cell_totals *totals, uint8_t *levels_out,
+                                            int32_t max_breakpoints, void *workspace, size_t workspace_bytes,
+                                            sprout_stream stream) {
+    return simulate_impl(problem, solution, trace, cost, totals, levels_out, max_breakpoints, workspace,
+                         workspace_bytes, stream, nullptr);
 }
 
 static sprout_status n4_args(const sprout_lp_problem *problem, const sprout_lp_solution *solution,

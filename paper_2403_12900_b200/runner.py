@@ -107,7 +107,8 @@ class Sweep:
         prof = None
         if profile:
             prof = torch.zeros((self.dp.cells, 2, self.prob_host.n), dtype=torch.float64, device=self.device)
-        S.simulate_closed_loop_q(self.dp, window, q_interval, self.trace, self.cost, self.sol, self.totals, prof, stream)
+        S.simulate_closed_loop_q(self.dp, window, q_interval, self.trace, self.cost, self.sol, self.totals, self.ws,
+                                 prof, stream)
         return prof
 
     def evaluation_q(self, interval_hours: float, beta: float, theta: float, grace_hours: float, fallback: int,

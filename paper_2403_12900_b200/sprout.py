@@ -109,7 +109,7 @@ class EvaluatorProblem(C.Structure):
 
 _lib.sprout_evaluator_sweep.argtypes = [_P(EvaluatorProblem), _vp, _vp]
 _lib.sprout_simulate_closed_loop.argtypes = [_P(LpProblem), C.c_int32, _P(Trace), _P(CostModel), _P(LpSolution),
-                                             _P(CellTotals), _vp, _vp]
+                                             _P(CellTotals), _vp, _vp, C.c_size_t, _vp]
 _lib.sprout_solve_scheme.argtypes = [_P(LpProblem), C.c_int32, C.c_int32, _P(LpSolution), _vp]
 _lib.sprout_static_grid_size.argtypes = [C.c_int32, C.c_int32]
 _lib.sprout_static_grid_size.restype = C.c_int64
@@ -359,11 +359,12 @@ def evaluator_sweep(k2: torch.Tensor, k2_max: torch.Tensor, n_intervals: int, in
 
 
 def simulate_closed_loop(prob: DeviceProblem, window: int, trace: DeviceTrace, cost: CostModel, sol: Solution,
-                         totals: Totals, profile_out: Optional[torch.Tensor] = None, stream=None) -> None:
+                         totals: Totals, ws: torch.Tensor, profile_out: Optional[torch.Tensor] = None,
+                         stream=None) -> None:
     p, t, s, tt = prob.c(), trace.c(), sol.c(), totals.c()
     _check("sprout_simulate_closed_loop",
            _lib.sprout_simulate_closed_loop(C.byref(p), int(window), C.byref(t), C.byref(cost), C.byref(s),
-                                            C.byref(tt), _ptr(profile_out), _stream(stream)))
+                                            C.byref(tt), _ptr(profile_out), _ptr(ws), ws.numel(), _stream(stream)))
 
 
 def check_cells(prob: DeviceProblem, sol: Solution, stream=None) -> int:
@@ -457,7 +458,7 @@ def simulate_oracle_scheme(prob: DeviceProblem, trace: DeviceTrace, cost: CostMo
 _lib.sprout_evaluation_q.argtypes = [_P(EvaluatorProblem), _P(LpProblem), _P(Trace), _P(CostModel), C.c_int32,
                                      _vp, _vp, _vp]
 _lib.sprout_simulate_closed_loop_q.argtypes = [_P(LpProblem), C.c_int32, _vp, _P(Trace), _P(CostModel),
-                                               _P(LpSolution), _P(CellTotals), _vp, _vp]
+                                               _P(LpSolution), _P(CellTotals), _vp, _vp, C.c_size_t, _vp]
 
 
 def evaluation_q(prob: DeviceProblem, trace: DeviceTrace, cost: CostModel, k2: torch.Tensor, k2_max: torch.Tensor,
@@ -474,9 +475,10 @@ def evaluation_q(prob: DeviceProblem, trace: DeviceTrace, cost: CostModel, k2: t
 
 
 def simulate_closed_loop_q(prob: DeviceProblem, window: int, q_interval: Optional[torch.Tensor], trace: DeviceTrace,
-                           cost: CostModel, sol: Solution, totals: Totals, profile_out: Optional[torch.Tensor] = None,
-                           stream=None) -> None:
+                           cost: CostModel, sol: Solution, totals: Totals, ws: torch.Tensor,
+                           profile_out: Optional[torch.Tensor] = None, stream=None) -> None:
     p, t, s, tt = prob.c(), trace.c(), sol.c(), totals.c()
     _check("sprout_simulate_closed_loop_q",
            _lib.sprout_simulate_closed_loop_q(C.byref(p), int(window), _ptr(q_interval), C.byref(t), C.byref(cost),
-                                              C.byref(s), C.byref(tt), _ptr(profile_out), _stream(stream)))
+                                              C.byref(s), C.byref(tt), _ptr(profile_out), _ptr(ws), ws.numel(),
+                                              _stream(stream)))
