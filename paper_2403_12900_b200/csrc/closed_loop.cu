@@ -119,6 +119,7 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
     __shared__ int ml_s, ok_s, act_s, seg_ok_s, done_s;
     __shared__ uint32_t seen[N];                             // level-L requests scanned so far (from the end)
     __shared__ uint32_t wtot[kClWarps][N];                   // per-warp counts of a piece
+    __shared__ uint32_t wsuf[kClWarps][N];                   // level-L requests after warp w (later warps + pieces)
     __shared__ int part[kClWarps][N * NCM * 2];              // per-warp window deltas of the interval
     const int W = a.W, NC = a.NC;
     uint32_t *ring = dyn, *scr = dyn + (size_t)N * W;
@@ -128,27 +129,57 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
     const CostConst &cost = a.cost;
     if (tid < N) { head[tid] = 0; size[tid] = 0; }
     for (int i = tid; i < N * NCM * 2; i += kClThreads) (&wsum[0][0][0])[i] = 0ull;
+    // the chain's constants (thread 0 solves the LPs) and the first interval's inputs
+    double pe[N], pp[N], qc[N], kmin_r = 0.0, kmax_r = 0.0, xi_j = 0.0;
+    if (tid == 0) {
+#pragma unroll
+        for (int L = 0; L < N; ++L) { pe[L] = a.e[(int64_t)r * N + L]; pp[L] = a.p[(int64_t)r * N + L]; qc[L] = a.q[(int64_t)r * N + L]; }
+        kmin_r = a.kmin[r]; kmax_r = a.kmax[r]; xi_j = a.xi[j];
+    }
+    const int64_t sfirst = (int64_t)r * a.T - a.first_segment;
+    int64_t nx0 = a.seg_offsets[sfirst], nx1 = a.seg_offsets[sfirst + 1];
+    double nk0 = tid == 0 ? a.k0[(int64_t)r * a.T] : 0.0;
+    double nq[N];
+#pragma unroll
+    for (int L = 0; L < N; ++L) nq[L] = (tid == 0 && a.q_seg) ? a.q_seg[(int64_t)r * a.T * N + L] : 0.0;
     __syncthreads();
     for (int64_t t = 0; t < a.T; ++t) {
         const int64_t s = (int64_t)r * a.T + t;          // global segment (k0, profiles)
         const int64_t sl = s - a.first_segment;          // local segment (offsets, outputs)
-        const int64_t s0 = a.seg_offsets[sl], s1 = a.seg_offsets[sl + 1];
+        const int64_t s0 = nx0, s1 = nx1;
+        const double k0_s = nk0;
+        double qv[N];
+#pragma unroll
+        for (int L = 0; L < N; ++L) qv[L] = a.q_seg ? nq[L] : qc[L];
+        if (t + 1 < a.T) {   // the next interval's inputs, one interval ahead
+            nx0 = s1;
+            nx1 = a.seg_offsets[sl + 2];
+            if (tid == 0) {
+                nk0 = a.k0[s + 1];
+                if (a.q_seg) {
+#pragma unroll
+                    for (int L = 0; L < N; ++L) nq[L] = a.q_seg[(s + 1) * N + L];
+                }
+            }
+        }
         // ---- the interval's LP with the closed-loop profile ----
         if (tid == 0) {
             const int64_t cell = sl * a.X + j;
-            const double *qrow = a.q_seg ? a.q_seg + s * N : a.q + (int64_t)r * N;
             double e[N], p[N], q[N];
 #pragma unroll
             for (int L = 0; L < N; ++L) {
-                q[L] = qrow[L];
+                q[L] = qv[L];
                 unsigned long long m = 0;
-                for (int cc = 0; cc < NC; ++cc) m += wsum[L][cc][0];
+#pragma unroll
+                for (int cc = 0; cc < NCM; ++cc) m += cc < NC ? wsum[L][cc][0] : 0ull;
                 if (m == 0) {
-                    e[L] = a.e[(int64_t)r * N + L];
-                    p[L] = a.p[(int64_t)r * N + L];
+                    e[L] = pe[L];
+                    p[L] = pp[L];
                 } else {
                     double se = 0.0, sp = 0.0;
-                    for (int cc = 0; cc < NC; ++cc) {
+#pragma unroll
+                    for (int cc = 0; cc < NCM; ++cc) {
+                        if (cc >= NC) break;
                         const double nc = (double)wsum[L][cc][0], kc = (double)wsum[L][cc][1];
                         se = __dadd_rn(se, __dadd_rn(__dmul_rn(nc, cost.ef[cc][L]), __dmul_rn(kc, cost.et[cc][L])));
                         sp = __dadd_rn(sp, __dadd_rn(__dmul_rn(nc, cost.pf[cc][L]), __dmul_rn(kc, cost.pt[cc][L])));
@@ -162,7 +193,7 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
                 }
             }
             LpCell<N> o;
-            lp_cell<N>(a.k0[s], a.kmin[r], a.kmax[r], a.xi[j], e, p, q, a.k1, a.pue, 0, 0, j, o);
+            lp_cell<N>(k0_s, kmin_r, kmax_r, xi_j, e, p, q, a.k1, a.pue, 0, 0, j, o);
 #pragma unroll
             for (int i = 0; i < N; ++i) a.x[cell * N + i] = o.x[i];
             a.objective[cell] = o.objective;
@@ -209,54 +240,69 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
                 const bool any = c0 + 8 > s0 && c0 < s1;
                 Chunk<N> ch;
                 load_chunk<N>(a, c0, any, ch);
-                uint32_t lv = 0u, valid = 0u;
-                uint32_t lc[N];
-#pragma unroll
-                for (int L = 0; L < N; ++L) lc[L] = 0u;
+                // valid requests of the chunk: inside [s0, s1) (a bit range) with a class < NC
+                uint32_t valid;
+                {
+                    const int64_t lo = min(max(s0 - c0, (int64_t)0), (int64_t)8), hi = min(max(s1 - c0, (int64_t)0), (int64_t)8);
+                    valid = ((1u << (uint32_t)hi) - 1u) & ~((1u << (uint32_t)lo) - 1u);
+                }
+                uint32_t lv = 0u;
+                uint64_t pk = 0ull;   // per-level counts of the chunk, one byte per level
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const int64_t g = c0 + k;
                     const uint32_t fb = flag_byte(ch.fw, k);
-                    const bool v = any && g >= s0 && g < s1 && ((fb >> 1) & 3u) < (uint32_t)NC;
+                    if (a.flags && ((fb >> 1) & 3u) >= (uint32_t)NC) valid &= ~(1u << k);
                     const int L = cl_level<N>(ch.w[k], T, ml, fb & 1u);
-                    valid |= v ? (1u << k) : 0u;
                     lv |= (uint32_t)L << (4 * k);
-#pragma unroll
-                    for (int LL = 0; LL < N; ++LL) lc[LL] += (v && LL == L) ? 1u : 0u;
+                    pk += ((valid >> k) & 1u) ? (1ull << (8 * L)) : 0ull;
                 }
-                // requests of each level in LATER threads of the piece (suffix scan)
+                // requests of each level in LATER threads of the warp (suffix scan)
                 uint32_t after[N];
 #pragma unroll
                 for (int L = 0; L < N; ++L) {
-                    uint32_t x = lc[L];
+                    const uint32_t c = (uint32_t)(pk >> (8 * L)) & 0xFFu;
+                    uint32_t x = c;
 #pragma unroll
                     for (int d = 1; d < 32; d <<= 1) {
                         const uint32_t y = __shfl_down_sync(0xFFFFFFFFu, x, d);
                         if (lane + d < 32) x += y;
                     }
-                    after[L] = x - lc[L];
+                    after[L] = x - c;
                     if (lane == 0) wtot[warp][L] = x;
                 }
                 __syncthreads();
-                uint32_t ptot[N];
+                // warp 0: per (warp, level) the requests after that warp (later warps of the
+                // piece + later pieces), the running totals and the stop test
+                if (warp == 0) {
+                    uint32_t all_done = 1u;
+                    if (lane < N) {
+                        const int L = lane;
+                        uint32_t run = seen[L];
 #pragma unroll
-                for (int L = 0; L < N; ++L) {
-                    uint32_t b = 0u, pt = 0u;
-#pragma unroll
-                    for (int w2 = 0; w2 < kClWarps; ++w2) {
-                        const uint32_t v = wtot[w2][L];
-                        b += w2 > warp ? v : 0u;
-                        pt += v;
+                        for (int w2 = kClWarps - 1; w2 >= 0; --w2) {
+                            wsuf[w2][L] = run;
+                            run += wtot[w2][L];
+                        }
+                        seen[L] = run;
+                        if (((act_s >> L) & 1) && run < (uint32_t)W) all_done = 0u;
                     }
-                    after[L] += b + seen[L];
-                    ptot[L] = pt;
+                    all_done = __all_sync(0xFFFFFFFFu, all_done != 0u) ? 1u : 0u;
+                    if (lane == 0) done_s = (int)all_done;
                 }
-                // the thread's requests from the latest: reverse rank = level-L requests after it
-                if (valid) {
+                __syncthreads();
+#pragma unroll
+                for (int L = 0; L < N; ++L) after[L] += wsuf[warp][L];
+                // the thread's requests from the latest: reverse rank = level-L requests after it;
+                // only levels whose window is not yet full need ranks
+                uint32_t need = 0u;
+#pragma unroll
+                for (int L = 0; L < N; ++L) need |= (after[L] < (uint32_t)W) ? (1u << L) : 0u;
+                if (valid && need) {
 #pragma unroll
                     for (int k = 7; k >= 0; --k) {
                         if (!((valid >> k) & 1u)) continue;
                         const int L = (int)((lv >> (4 * k)) & 15u);
+                        if (!((need >> L) & 1u)) continue;
                         uint32_t rho = 0u, tl = 0u;
 #pragma unroll
                         for (int LL = 0; LL < N; ++LL)
@@ -264,19 +310,9 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
                         if (rho < (uint32_t)W) scr[(size_t)L * W + rho] = (((flag_byte(ch.fw, k) >> 1) & 3u) << 16) | tl;
                     }
                 }
-                __syncthreads();   // seen / wtot are read above before they change
-                if (tid == 0) {
-                    int done = 1;
-#pragma unroll
-                    for (int L = 0; L < N; ++L) {
-                        seen[L] += ptot[L];
-                        if (((act_s >> L) & 1) && seen[L] < (uint32_t)W) done = 0;
-                    }
-                    done_s = done;
-                }
-                __syncthreads();
                 if (done_s) break;
             }
+            __syncthreads();   // every scratch entry written
         }
         // ---- append the scratch entries (forward order) to the rings, evicting the oldest ----
         int dn[N][NCM], dk[N][NCM];
@@ -290,7 +326,9 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
                 const uint32_t k = min(seen[L], (uint32_t)W);
                 const uint32_t h = (uint32_t)head[L], sz = (uint32_t)size[L];
                 for (uint32_t i = tid; i < k; i += kClThreads) {
-                    const uint32_t pos = (h + sz + i) % (uint32_t)W;
+                    uint32_t pos = h + sz + i;   // < 3W
+                    pos = pos >= (uint32_t)W ? pos - (uint32_t)W : pos;
+                    pos = pos >= (uint32_t)W ? pos - (uint32_t)W : pos;
                     uint32_t *rp = ring + (size_t)L * W + pos;
                     if (sz + i >= (uint32_t)W) {   // the slot's old entry is the oldest: it leaves
                         const uint32_t old = *rp;
@@ -337,7 +375,8 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
             const uint32_t k = min(seen[tid], (uint32_t)W);
             const uint32_t sz = (uint32_t)size[tid];
             const uint32_t ev = sz + k > (uint32_t)W ? sz + k - (uint32_t)W : 0u;
-            head[tid] = (int)(((uint32_t)head[tid] + ev) % (uint32_t)W);
+            const uint32_t hh = (uint32_t)head[tid] + ev;
+            head[tid] = (int)(hh >= (uint32_t)W ? hh - (uint32_t)W : hh);
             size[tid] = (int)min(sz + k, (uint32_t)W);
         }
         __syncthreads();
