@@ -116,10 +116,9 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
     __shared__ unsigned long long wsum[N][NCM][2];          // window: requests, tokens per (level, class)
     __shared__ int head[N], size[N];
     __shared__ uint32_t thr_s[N > 1 ? N - 1 : 1];
-    __shared__ int ml_s, ok_s, act_s, seg_ok_s, done_s;
+    __shared__ int ml_s, ok_s, act_s, seg_ok_s;
     __shared__ uint32_t seen[N];                             // level-L requests scanned so far (from the end)
-    __shared__ uint32_t wtot[kClWarps][N];                   // per-warp counts of a piece
-    __shared__ uint32_t wsuf[kClWarps][N];                   // level-L requests after warp w (later warps + pieces)
+    __shared__ uint32_t wtot[2][kClWarps][N];                // per-warp counts of a piece (double-buffered by piece parity)
     __shared__ int part[kClWarps][N * NCM * 2];              // per-warp window deltas of the interval
     const int W = a.W, NC = a.NC;
     uint32_t *ring = dyn, *scr = dyn + (size_t)N * W;
@@ -162,6 +161,13 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
                 }
             }
         }
+        // the interval's last piece (the backward scan's first): warps 1.. load it and
+        // take its draws while thread 0 solves the LP (warp 0 loads it after)
+        const int64_t e_al = (s1 + 7) & ~(int64_t)7;
+        Chunk<N> ch;
+        const int64_t c00 = e_al - kClPiece + 8 * (int64_t)tid;
+        const bool any0 = s0 <= s1 && c00 + 8 > s0 && c00 < s1 && s1 <= a.n_requests && s0 >= 0;
+        if (warp != 0) load_chunk<N>(a, c00, any0, ch);
         // ---- the interval's LP with the closed-loop profile ----
         if (tid == 0) {
             const int64_t cell = sl * a.X + j;
@@ -231,15 +237,15 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
         const int ml = ml_s;
         // ---- backward scan: the interval's last W requests of every reachable level ----
         if (run) {
-            const int64_t e_al = (s1 + 7) & ~(int64_t)7, b_al = s0 & ~(int64_t)7;
+            if (warp == 0) load_chunk<N>(a, c00, any0, ch);
+            const int64_t b_al = s0 & ~(int64_t)7;
             const int n_pieces = (int)((e_al - b_al + kClPiece - 1) / kClPiece);
+            uint32_t seen_r = 0u;   // lane L < N: level-L requests scanned so far (every warp the same)
             for (int pi = 0; pi < n_pieces; ++pi) {
                 const int64_t base = e_al - (int64_t)(pi + 1) * kClPiece;
                 prefetch_piece<N>(a, base - 2 * (int64_t)kClPiece, s1, tid);
                 const int64_t c0 = base + 8 * (int64_t)tid;
-                const bool any = c0 + 8 > s0 && c0 < s1;
-                Chunk<N> ch;
-                load_chunk<N>(a, c0, any, ch);
+                if (pi > 0) load_chunk<N>(a, c0, c0 + 8 > s0 && c0 < s1, ch);
                 // valid requests of the chunk: inside [s0, s1) (a bit range) with a class < NC
                 uint32_t valid;
                 {
@@ -258,6 +264,7 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
                 }
                 // requests of each level in LATER threads of the warp (suffix scan)
                 uint32_t after[N];
+                uint32_t (*wt)[N] = wtot[pi & 1];
 #pragma unroll
                 for (int L = 0; L < N; ++L) {
                     const uint32_t c = (uint32_t)(pk >> (8 * L)) & 0xFFu;
@@ -268,30 +275,24 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
                         if (lane + d < 32) x += y;
                     }
                     after[L] = x - c;
-                    if (lane == 0) wtot[warp][L] = x;
+                    if (lane == 0) wt[warp][L] = x;
                 }
                 __syncthreads();
-                // warp 0: per (warp, level) the requests after that warp (later warps of the
-                // piece + later pieces), the running totals and the stop test
-                if (warp == 0) {
-                    uint32_t all_done = 1u;
-                    if (lane < N) {
-                        const int L = lane;
-                        uint32_t run = seen[L];
+                // lane L of every warp: level-L requests in later warps of the piece, and the
+                // piece total; then the stop test (identical in every warp)
+                uint32_t later = 0u, ptot = 0u;
+                if (lane < N) {
 #pragma unroll
-                        for (int w2 = kClWarps - 1; w2 >= 0; --w2) {
-                            wsuf[w2][L] = run;
-                            run += wtot[w2][L];
-                        }
-                        seen[L] = run;
-                        if (((act_s >> L) & 1) && run < (uint32_t)W) all_done = 0u;
+                    for (int w2 = 0; w2 < kClWarps; ++w2) {
+                        const uint32_t v = wt[w2][lane];
+                        later += w2 > warp ? v : 0u;
+                        ptot += v;
                     }
-                    all_done = __all_sync(0xFFFFFFFFu, all_done != 0u) ? 1u : 0u;
-                    if (lane == 0) done_s = (int)all_done;
                 }
-                __syncthreads();
 #pragma unroll
-                for (int L = 0; L < N; ++L) after[L] += wsuf[warp][L];
+                for (int L = 0; L < N; ++L) after[L] += __shfl_sync(0xFFFFFFFFu, later + seen_r, L);
+                seen_r += ptot;
+                const bool done = __all_sync(0xFFFFFFFFu, lane >= N || !((act_s >> lane) & 1) || seen_r >= (uint32_t)W);
                 // the thread's requests from the latest: reverse rank = level-L requests after it;
                 // only levels whose window is not yet full need ranks
                 uint32_t need = 0u;
@@ -310,9 +311,10 @@ __global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_cons
                         if (rho < (uint32_t)W) scr[(size_t)L * W + rho] = (((flag_byte(ch.fw, k) >> 1) & 3u) << 16) | tl;
                     }
                 }
-                if (done_s) break;
+                if (done) break;
             }
-            __syncthreads();   // every scratch entry written
+            if (warp == 0 && lane < N) seen[lane] = seen_r;
+            __syncthreads();   // every scratch entry written, seen final
         }
         // ---- append the scratch entries (forward order) to the rings, evicting the oldest ----
         int dn[N][NCM], dk[N][NCM];
