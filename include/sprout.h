@@ -345,6 +345,25 @@ sprout_status sprout_evaluator_sweep(const sprout_evaluator_problem *problem, do
                                      sprout_stream stream);
 
 /* ---------------------------------------------------------------------- */
+/* Per-request fp64 accounting (a cross-check of sprout_simulate_trace's
+ * closed form).  For every cell: each request's level by
+ * the a6 rule straight from the cell's thresholds at its Philox word
+ * (reading L10; opted-out requests L0; invalid classes skipped), its
+ * Eq. 1 energy E = ef + et*tok, time T = pf + pt*tok (
+ * reading L11), carbon k0*PUE*E + k1*T (reading L2) and quality q[level]
+ * (reading L15), summed in fp64 per thread in request order and then by a
+ * fixed warp-shuffle / block tree -- deterministic.  energy_kwh, time_s,
+ * carbon_g, quality: device, [cells] fp64, caller-owned, written for every
+ * cell (0 for invalid cells and segments with invalid offsets).  Equal to
+ * sprout_simulate_trace's totals within fp64 summation error (the tests use
+ * 1e-12 relative).  One CTA per segment; every cell re-reads the segment:
+ * a verification mode, not the timed path.  Errors: INVALID_ARGUMENT (as
+ * sprout_simulate_trace); CUDA. */
+sprout_status sprout_cell_totals_fp64(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                      const sprout_trace *trace, const sprout_cost_model *cost, double *energy_kwh,
+                                      double *time_s, double *carbon_g, double *quality, sprout_stream stream);
+
+/* ---------------------------------------------------------------------- */
 /* Closed-loop profiles (reading L20).  P:183: e and p
  * are "the average energy consumption and processing time for recent
  * requests at each level".  Steps 1-2 as one causal scan per (region, xi)

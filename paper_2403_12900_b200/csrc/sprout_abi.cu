@@ -354,6 +354,40 @@ sprout_status sprout_simulate_trace_bounded(const sprout_lp_problem *problem, co
                          workspace_bytes, stream, nullptr);
 }
 
+sprout_status sprout_cell_totals_fp64(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
+                                      const sprout_trace *trace, const sprout_cost_model *cost, double *energy_kwh,
+                                      double *time_s, double *carbon_g, double *quality, sprout_stream stream) {
+    sprout_status st = validate_problem(problem);
+    if (st == SPROUT_OK) st = validate_solution(problem, solution);
+    if (st == SPROUT_OK) st = validate_trace(problem, trace);
+    if (st == SPROUT_OK) st = validate_cost(cost);
+    if (st != SPROUT_OK) return st;
+    if (!energy_kwh || !time_s || !carbon_g || !quality || !aligned(energy_kwh, 8) || !aligned(time_s, 8) ||
+        !aligned(carbon_g, 8) || !aligned(quality, 8))
+        return SPROUT_ERR_INVALID_ARGUMENT;
+    F64Args a{};
+    a.n = problem->n_levels; a.X = problem->n_xi; a.NC = cost->n_classes;
+    a.T = problem->n_intervals; a.first_segment = problem->first_segment; a.n_segments = problem->n_segments;
+    a.profile_per_interval = problem->profile_per_interval;
+    a.k0 = problem->k0; a.q = problem->q; a.k1 = problem->k1; a.pue = problem->pue;
+    a.threshold = solution->threshold; a.max_level = solution->max_level; a.cell_status = solution->cell_status;
+    a.n_requests = trace->n_requests; a.first_request = trace->first_request; a.seg_offsets = trace->seg_offsets;
+    a.tokens = trace->tokens; a.pitch = trace->plane_pitch; a.flags = trace->flags;
+    {
+        uint32_t k0 = (uint32_t)cost->seed, k1 = (uint32_t)(cost->seed >> 32);
+        for (int r = 0; r < 10; ++r) { a.rk0[r] = k0; a.rk1[r] = k1; k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    }
+    std::memcpy(a.cost.ef, cost->ef, sizeof(cost->ef));
+    std::memcpy(a.cost.et, cost->et, sizeof(cost->et));
+    std::memcpy(a.cost.pf, cost->pf, sizeof(cost->pf));
+    std::memcpy(a.cost.pt, cost->pt, sizeof(cost->pt));
+    a.energy = energy_kwh; a.time_s = time_s; a.carbon = carbon_g; a.quality = quality;
+    int launches = 0;
+    st = cuda_status(launch_fp64_cells(a, reinterpret_cast<cudaStream_t>(stream), &launches));
+    if (st == SPROUT_OK) g_last_launches = launches;
+    return st;
+}
+
 static sprout_status n4_args(const sprout_lp_problem *problem, const sprout_lp_solution *solution,
                              const sprout_trace *trace, const sprout_cost_model *cost, N4Args &a) {
     sprout_status st = validate_problem(problem);

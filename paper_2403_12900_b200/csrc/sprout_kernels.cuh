@@ -184,6 +184,8 @@ struct SimArgs {
     double *seg_base;
     uint32_t *trace_status;
     uint8_t *levels_out;
+    uint8_t *bins_out;         // verify mode: every request's histogram bin as the streaming kernel found it
+    int bins_ready;            // bins_out was written by the streaming kernel (levels_kernel reads it)
     // workspace
     uint32_t *queue;           // work counter
     int32_t *seg_meta;         // [n_segments] K, -1 slow, -2 bad offsets
@@ -230,6 +232,26 @@ struct GenArgs {
     uint8_t *flags;
 };
 
+struct F64Args {                // per-request fp64 accounting mode (fp64_check.cu)
+    int n, X, NC;
+    int64_t T, first_segment, n_segments;
+    int profile_per_interval;
+    const double *k0, *q;
+    double k1, pue;
+    const uint32_t *threshold;
+    const uint8_t *max_level, *cell_status;
+    int64_t n_requests;
+    uint64_t first_request;
+    const int64_t *seg_offsets;
+    const uint16_t *tokens;
+    int64_t pitch;
+    const uint8_t *flags;
+    uint32_t rk0[10], rk1[10];
+    CostConst cost;
+    double *energy, *time_s, *carbon, *quality;
+};
+
+cudaError_t launch_fp64_cells(const F64Args &a, cudaStream_t stream, int *launches);
 cudaError_t launch_lp_solve(const LpArgs &a, cudaStream_t stream, int *launches);
 bool make_sim_plan(int n, int X, int NC, SimPlan *plan, int max_keys = 0);
 size_t sim_workspace_bytes(const SimPlan &plan, int64_t n_segments);

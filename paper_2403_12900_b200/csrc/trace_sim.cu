@@ -1019,7 +1019,7 @@ __device__ __forceinline__ void readout(const SimArgs &a, const WarpSmem &W, int
 // each lane draws its request's word, finds its bin and adds it into its own
 // lane-private row (tokens >= 4096 go to the 64-bit accumulators).  All lanes
 // work at once, so a short segment does not serialise on two lanes.
-template <int N, bool FLAGS, int MODE>
+template <int N, bool FLAGS, int MODE, bool VB>
 __device__ __forceinline__ void process_ends(const SimArgs &a, const WarpSmem &W, int64_t s0, int64_t s1, int P,
                                              LutGeom geo, uint32_t &err) {
     constexpr int NW = Words<N>::NW;
@@ -1046,6 +1046,7 @@ __device__ __forceinline__ void process_ends(const SimArgs &a, const WarpSmem &W
     } else {
         bin = find_bin(W.keys, P, w);
     }
+    if (VB) a.bins_out[r] = (uint8_t)bin;   // verify mode: the bin this kernel found
     int entry = bin;
     if (FLAGS) {
         const uint32_t fb = a.flags[r];
@@ -1109,7 +1110,7 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
 // the integer rounds with the shared-memory read-modify-write chain.  The
 // (at most two) partial groups at the segment's ends take the careful
 // 64-bit path.
-template <int N, bool FLAGS, int MODE>
+template <int N, bool FLAGS, int MODE, bool VB>
 __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem &W, int64_t s0, int64_t s1, int P,
                                                LutGeom geo, uint32_t &err) {
     if (s1 <= s0) return;
@@ -1122,7 +1123,7 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
     };
     for (int it = 1; it < kPrefetchIters; ++it)
         if (gf + lane + 32 * it < ge) prefetch_group(gf + lane + 32 * it);
-    process_ends<N, FLAGS, MODE>(a, W, s0, s1, P, geo, err);
+    process_ends<N, FLAGS, MODE, VB>(a, W, s0, s1, P, geo, err);
     constexpr uint32_t rowbytes = Words<N>::NP * 256;
     const uint32_t lane_base = smem_u32(W.hist) + lane * 8u;
     const uint32_t discard_row = lane_base + (uint32_t)(a.NC * a.nb) * rowbytes;
@@ -1190,6 +1191,15 @@ __device__ __forceinline__ void stream_segment(const SimArgs &a, const WarpSmem 
 #pragma unroll
         for (int k = 0; k < 8; ++k)
             row.v[k] = row_of<FLAGS>(oc[b].v[k], g[b].f, k, pin_row, class_bytes, a.NC, discard_row, err);
+        if (VB) {   // verify mode: the eight draw bins this kernel looked up, one 8-byte store
+            uint32_t lo8 = 0u, hi8 = 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                lo8 |= ((oc[b].v[k] - lane_base) / rowbytes) << (8 * k);
+                hi8 |= ((oc[b].v[4 + k] - lane_base) / rowbytes) << (8 * k);
+            }
+            reinterpret_cast<uint2 *>(a.bins_out)[v0 + 32 * (int64_t)i] = make_uint2(lo8, hi8);
+        }
         uint32_t en = 0u;
         const uint32_t acc =
             update_fast<N, FLAGS, MODE>(g[b], row, lane_base, wq[b], W, P, geo, rowbytes, oc[b ^ 1], en);
@@ -1278,7 +1288,7 @@ __device__ __forceinline__ void stream_segment_k0(const SimArgs &a, const WarpSm
     __syncwarp();
 }
 
-template <int N, bool FLAGS>
+template <int N, bool FLAGS, bool VB>
 __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __grid_constant__ SimArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ CostConst cost;   // per-launch coefficients (dynamic [class][level] indexing)
@@ -1415,9 +1425,9 @@ __global__ void __launch_bounds__(32 * kMaxTraceWarps, 1) trace_kernel(const __g
         } else if (a.lut && K >= kLutMinKeys && s1 - s0 >= kLutMinRequests) {
             const LutGeom geo = lut_geometry(W, K);
             build_lut(W, K, geo, Words<N>::NP * 256);
-            stream_segment<N, FLAGS, kModeLut>(a, W, s0, s1, P, geo, err);
+            stream_segment<N, FLAGS, kModeLut, VB>(a, W, s0, s1, P, geo, err);
         } else {
-            stream_segment<N, FLAGS, kModeSearch>(a, W, s0, s1, P, LutGeom{0u, 32 - kLutBits, 0u}, err);
+            stream_segment<N, FLAGS, kModeSearch, VB>(a, W, s0, s1, P, LutGeom{0u, 32 - kLutBits, 0u}, err);
         }
         __syncwarp();
         // the next segment's first groups into L2 while this one's epilogue
@@ -2206,7 +2216,9 @@ __global__ void __launch_bounds__(256) levels_kernel(const __grid_constant__ Sim
                 bad = ((f >> 1) & 3) >= a.NC;
             }
             int bin = 0;
-            if (meta >= 0) {
+            if (meta > 0 && a.bins_ready) {
+                bin = a.bins_out[r];   // the bin the streaming kernel found (pinned requests: unused)
+            } else if (meta >= 0) {
                 const uint32_t *keys = a.seg_keys + sl * a.kcap;
                 for (int k = 0; k < meta; ++k) bin += (keys[k] < w) ? 1 : 0;
             }
@@ -2344,7 +2356,7 @@ template <int N, bool FLAGS>
 static cudaError_t launch_trace_t(SimArgs &a, const SimPlan &plan, cudaStream_t stream) {
     const int threads = plan.warps_per_cta * 32;
     const size_t smem = plan.warp_smem * plan.warps_per_cta;
-    auto kern = trace_kernel<N, FLAGS>;
+    auto kern = a.bins_out ? trace_kernel<N, FLAGS, true> : trace_kernel<N, FLAGS, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, sms = 148, per_sm = 1;
@@ -2362,7 +2374,12 @@ static cudaError_t launch_trace_t(SimArgs &a, const SimPlan &plan, cudaStream_t 
 
 template <int N>
 static cudaError_t launch_n(SimArgs &a, const SimPlan &plan, cudaStream_t stream, int *launches) {
-    cudaError_t e = (!kDisableX1 && trace_x1_supported(N, a.X, a.NC)) ? launch_trace_x1(a, stream)
+    const bool x1 = !kDisableX1 && trace_x1_supported(N, a.X, a.NC);
+    // verify mode on the breakpoint-histogram kernel: it writes every request's bin
+    // into row 0 of levels_out, and levels_kernel derives the levels from those bins
+    a.bins_out = (a.levels_out && !x1 && !(N == 3 && a.wide) && plan.kcap <= 254) ? a.levels_out : nullptr;
+    a.bins_ready = a.bins_out ? 1 : 0;
+    cudaError_t e = x1 ? launch_trace_x1(a, stream)
                   : (N == 3 && a.wide) ? launch_trace_wide(a, plan, stream)
                   : a.flags ? launch_trace_t<N, true>(a, plan, stream) : launch_trace_t<N, false>(a, plan, stream);
     if (e != cudaSuccess) return e;

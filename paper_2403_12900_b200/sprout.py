@@ -126,7 +126,8 @@ EXPORTS = ["sprout_solve_directives", "sprout_workspace_bytes", "sprout_simulate
            "sprout_select_static", "sprout_simulate_trace_bounded", "sprout_evaluator_sweep",
            "sprout_simulate_closed_loop", "sprout_request_outputs", "sprout_preference_stats",
            "sprout_normalized_preference", "sprout_oracle_scheme_workspace_bytes",
-           "sprout_simulate_oracle_scheme", "sprout_evaluation_q", "sprout_simulate_closed_loop_q"]
+           "sprout_simulate_oracle_scheme", "sprout_evaluation_q", "sprout_simulate_closed_loop_q",
+           "sprout_cell_totals_fp64"]
 
 # competing schemes, include/sprout.h SPROUT_SCHEME_*
 SCHEME_SPROUT, SCHEME_CO2_OPT, SCHEME_STATIC_GRID = 0, 1, 2
@@ -365,6 +366,23 @@ def simulate_closed_loop(prob: DeviceProblem, window: int, trace: DeviceTrace, c
     _check("sprout_simulate_closed_loop",
            _lib.sprout_simulate_closed_loop(C.byref(p), int(window), C.byref(t), C.byref(cost), C.byref(s),
                                             C.byref(tt), _ptr(profile_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+_lib.sprout_cell_totals_fp64.argtypes = [_P(LpProblem), _P(LpSolution), _P(Trace), _P(CostModel), _vp, _vp, _vp,
+                                         _vp, _vp]
+_lib.sprout_cell_totals_fp64.restype = C.c_int
+
+
+def cell_totals_fp64(prob: DeviceProblem, sol: Solution, trace: DeviceTrace, cost: CostModel, stream=None) -> dict:
+    """Per-request fp64 accounting (cross-check of the closed form): energy, time, carbon, quality per cell."""
+    out = {k: torch.zeros(prob.cells, dtype=torch.float64, device=trace.tokens.device)
+           for k in ("energy", "time", "carbon", "quality")}
+    p, s, t = prob.c(), sol.c(), trace.c()
+    _check("sprout_cell_totals_fp64",
+           _lib.sprout_cell_totals_fp64(C.byref(p), C.byref(s), C.byref(t), C.byref(cost), _ptr(out["energy"]),
+                                        _ptr(out["time"]), _ptr(out["carbon"]), _ptr(out["quality"]),
+                                        _stream(stream)))
+    return out
 
 
 def check_cells(prob: DeviceProblem, sol: Solution, stream=None) -> int:

@@ -15,7 +15,7 @@ LIB = os.path.join(ROOT, "paper_2403_12900_b200", "libsprout.so")
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(sprout_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(sprout_[a-z0-9_]+)\s*\(", src)))
 
 
 @pytest.fixture(scope="module")

@@ -502,3 +502,25 @@ def test_graph_captured_step_matches_eager(world):
             np.testing.assert_array_equal(got[k], want[k], err_msg=k)
         for k in ("energy", "time", "carbon", "quality", "group"):
             np.testing.assert_array_equal(got[k].view(np.uint64), want[k].view(np.uint64), err_msg=k)
+
+
+@pytest.mark.parametrize("name,kw", [("C2", dict(n_requests=200_000, n_intervals=48)),
+                                     ("C3", dict(n_requests=400_000, n_intervals=288)),
+                                     ("C4", dict(n_requests=1_000_000, n_intervals=48)),
+                                     ("C5", dict(n_requests=300_000, n_intervals=24, n_regions=6))])
+def test_fp64_per_request_mode_matches_closed_form(name, kw):
+    # Eq. 1 per request in fp64 + warp-shuffle / block tree sums (sprout_cell_totals_fp64)
+    # against the streaming kernel's closed form from exact integer statistics, and the
+    # oracle's sequential per-request fp64 sums: both within 1e-12 relative
+    w = synth.make_workload(name, **kw)
+    sh, toks, flags, got = run_full(w, levels=False)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=flags)
+    sw.solve()
+    f64 = S.cell_totals_fp64(sw.dp, sw.sol, sw.trace, sw.cost)
+    torch.cuda.synchronize()
+    sim = oracle_shard(w, sh, toks, flags)
+    X = w.prob.X
+    for k in ("energy", "time", "carbon", "quality"):
+        v = f64[k].cpu().numpy()
+        np.testing.assert_allclose(v, got[k].reshape(-1), rtol=1e-12, atol=1e-300, err_msg=k)
+        np.testing.assert_allclose(v, sim[k].reshape(-1), rtol=1e-12, atol=1e-300, err_msg=k)
