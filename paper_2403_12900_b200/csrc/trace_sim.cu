@@ -2441,8 +2441,15 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
     }
     a.wide = wide_applies(a, plan) ? 1 : 0;
 
-    // prep (also resets the queue and trace_status)
-    {
+    // prep (also resets the queue and trace_status).  The one-cell kernels need no
+    // breakpoints and check the offsets themselves: without verify mode they only
+    // need the two counters reset
+    if (!kDisableX1 && trace_x1_supported(plan.n, a.X, a.NC) && !a.levels_out) {
+        cudaError_t e = cudaMemsetAsync(a.queue, 0, 4, stream);
+        if (e == cudaSuccess) e = cudaMemsetAsync(a.trace_status, 0, 4, stream);
+        if (e != cudaSuccess) return e;
+        a.seg_meta = nullptr;
+    } else {
         int64_t blocks = (a.n_segments + kPrepWarps - 1) / kPrepWarps;
         if (blocks > 148 * 32) blocks = 148 * 32;
         if (blocks < 1) blocks = 1;

@@ -524,3 +524,20 @@ def test_fp64_per_request_mode_matches_closed_form(name, kw):
         v = f64[k].cpu().numpy()
         np.testing.assert_allclose(v, got[k].reshape(-1), rtol=1e-12, atol=1e-300, err_msg=k)
         np.testing.assert_allclose(v, sim[k].reshape(-1), rtol=1e-12, atol=1e-300, err_msg=k)
+
+
+@pytest.mark.parametrize("n,NC,flags", [(3, 2, True), (2, 1, False)])
+def test_x1_grouped_kernel_long_segment_chunks(n, NC, flags):
+    """Short segments on average take the grouped one-cell kernel (4 segments
+    per warp); one segment longer than a lane group's 2^19-request fold chunk
+    forces several folds while its group's neighbours finish early."""
+    w = _custom(n=n, X=1, NC=NC, flags=flags, N=1_500_000, T=900, R=2, xi=[0.4])
+    off = w.spec.seg_offsets
+    m = np.diff(off)
+    m[:] = 100
+    m[::11] = 0
+    m[17] = 1_200_000
+    m[18] = 5
+    off[1:] = np.cumsum(m)
+    assert off[-1] <= 1024 * len(m)
+    check_full(w)
