@@ -28,3 +28,13 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:trace_kernel -s 2 -c 1 -o gpurun_out/prof_$TAG python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_$TAG.log 2>&1; echo "ncu-full rc=$?"
 timeout 900 ncu --set full --clock-control none -k regex:'lp_solve|prep_kernel|reduce_stage' -s 6 -c 5 -o gpurun_out/prof_other_$TAG python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_other_$TAG.log 2>&1; echo "ncu-other rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:cl_window -c 1 -o gpurun_out/prof_cl_$TAG python bench.py --config C4 --closed-loop 1000 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_cl_$TAG.log 2>&1; echo "ncu-cl rc=$?"
+# summaries on the box (the .ncu-rep files are large; gpurun_out must stay < 64 MiB)
+for R in prof_$TAG prof_other_$TAG prof_cl_$TAG; do
+  [ -f gpurun_out/$R.ncu-rep ] || continue
+  python tools/ncu_summary.py gpurun_out/$R.ncu-rep > gpurun_out/${R}_summary.txt 2>&1
+  python tools/ncu_lines.py gpurun_out/$R.ncu-rep 60 > gpurun_out/${R}_lines.txt 2>&1
+  python tools/ncu_opmix.py gpurun_out/$R.ncu-rep > gpurun_out/${R}_opmix.txt 2>&1
+done
+ncu -i gpurun_out/prof_$TAG.ncu-rep --page raw --csv --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > gpurun_out/prof_${TAG}_traffic.csv 2>&1
+rm -f gpurun_out/prof_other_$TAG.ncu-rep gpurun_out/prof_cl_$TAG.ncu-rep
+du -sh gpurun_out

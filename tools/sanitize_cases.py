@@ -1,8 +1,9 @@
 """Small invocations of every kernel of the library, for compute-sanitizer
 (memcheck / racecheck / synccheck): the trace kernel (histogram path, C2
 shape with flags and 3 xi), the one-cell kernel (C1, C3 shape), the closed
-loop (+ q per epoch), the NEXT-4 kernels, the competing schemes and the
-evaluator sweep.  Usage: compute-sanitizer --tool T python tools/sanitize_cases.py"""
+loop (+ q per epoch), the NEXT-4 kernels, the competing schemes, the
+evaluator sweep, the grouped one-cell kernel (short segments, with and
+without verify mode) and the fp64 per-request accounting mode.  Usage: compute-sanitizer --tool T python tools/sanitize_cases.py"""
 import os
 import sys
 
@@ -22,7 +23,8 @@ def run(name, **kw):
     sh = synth.shard(w.spec, 1, 0)
     toks, fl = synth.host_trace(w.spec, sh)
     sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=fl)
-    sw.solve(); sw.simulate(levels=True); sw.reduce()
+    sw.solve(); sw.simulate(levels=True); sw.simulate(); sw.reduce()
+    S.cell_totals_fp64(sw.dp, sw.sol, sw.trace, sw.cost)
     sw.preference_stats(); sw.request_outputs(0); sw.oracle_scheme()
     q, _ = sw.evaluation_q(24.0 / (w.prob.T / 365) if w.prob.T >= 365 else 1.0, 0.028, 0.5, 6.0, 3, 100)
     sw.closed_loop(20, profile=True, q_interval=q); sw.reduce()
