@@ -433,6 +433,12 @@ def run_sprout(args):
         alg = algorithmic_bytes(w, sh) + sh.n_segments * P.X * (P.n * 8 + 8 + 8)
     sim_avg_ms = statistics.mean(sim_ms)
     sim_med_ms = statistics.median(sim_ms)
+    if world > 1:   # per-GPU average over the job: all ranks' bytes over the slowest rank's time
+        t = torch.tensor([float(alg)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        alg = float(t.item()) / world
+        sim_avg_ms = max_over_ranks(sim_avg_ms, dev)
+        sim_med_ms = max_over_ranks(sim_med_ms, dev)
     achieved = alg / (sim_avg_ms * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
