@@ -21,8 +21,9 @@
  * Conventions
  *   - Every array pointer inside the structs is a DEVICE pointer (cudaMalloc
  *     / torch CUDA tensor) owned by the caller, except where a function says
- *     HOST.  The library allocates nothing persistent and keeps no global
- *     state: calls are thread-safe and asynchronous on `stream`.
+ *     HOST.  The library allocates nothing persistent; its only state is a
+ *     thread-local launch counter (sprout_last_launch_count), so calls are
+ *     thread-safe and asynchronous on `stream`.
  *   - Host-checkable arguments are validated synchronously before anything
  *     is enqueued; a non-OK status means nothing was launched.
  *   - Data in device arrays is validated on the device, per cell
