@@ -161,3 +161,31 @@ def test_evaluation_q_and_closed_loop_q(name, kw, dt, grace, sample):
     np.testing.assert_array_equal(got["cnt"].reshape(-1, NC, n), want["cnt"])
     np.testing.assert_allclose(got["quality"].reshape(-1), want["quality"], rtol=FP_RTOL, atol=0)
     np.testing.assert_allclose(got["carbon"].reshape(-1), want["carbon"], rtol=FP_RTOL, atol=0)
+
+
+@pytest.mark.parametrize("n,NC,flags,W", [(1, 1, False, 3), (8, 1, False, 40), (4, 4, True, 25), (2, 3, True, 1)])
+def test_closed_loop_levels_classes_ragged(n, NC, flags, W):
+    """The chain kernel's other template instances (n = 1, n = 8, four
+    classes) on ragged intervals: empty ones, single requests, and one longer
+    than several scan pieces."""
+    from test_gpu_parity import _custom
+    w = _custom(n=n, X=3, NC=NC, flags=flags, N=30_000, T=30, R=2, xi=[0.0, 0.35, 1.0])
+    off = w.spec.seg_offsets
+    m = np.diff(off)
+    m[::5] = 0
+    m[3] = 1
+    m[8] = 9000
+    off[1:] = np.cumsum(m)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, fl = synth.host_trace(w.spec, sh)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=fl)
+    prof = sw.closed_loop(W, profile=True)
+    torch.cuda.synchronize()
+    got = sw.host()
+    want = oracle.closed_loop(w.prob, w.cost, W, w.spec.seg_offsets, toks, fl)
+    np.testing.assert_array_equal(prof.cpu().numpy().view(np.uint64), want["profile"].view(np.uint64))
+    np.testing.assert_array_equal(got["x"].view(np.uint64), want["x"].view(np.uint64))
+    np.testing.assert_array_equal(got["cnt"].reshape(-1, NC, n), want["cnt"])
+    np.testing.assert_array_equal(got["tok"].reshape(-1, NC, n), want["tok"])
+    for k in ("energy", "time", "carbon", "quality"):
+        np.testing.assert_allclose(got[k].reshape(-1), want[k], rtol=FP_RTOL, atol=0, err_msg=k)
