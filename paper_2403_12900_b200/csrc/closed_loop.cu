@@ -29,7 +29,13 @@
 
 namespace sprout {
 
-constexpr int kClThreads = 256;
+#ifndef SPROUT_CL_THREADS
+#define SPROUT_CL_THREADS 256
+#endif
+#ifndef SPROUT_CL_MINB
+#define SPROUT_CL_MINB 2
+#endif
+constexpr int kClThreads = SPROUT_CL_THREADS;
 constexpr int kClWarps = kClThreads / 32;
 constexpr int kClPiece = 8 * kClThreads;   // requests per piece: 8 per thread
 
@@ -111,7 +117,7 @@ __device__ __forceinline__ void prefetch_piece(const ClosedArgs &a, int64_t p0, 
 // are known they are exactly the open-loop totals of those thresholds, and
 // the caller (sprout_abi.cu) runs the streaming simulate kernel for them.
 template <int N, int NCM>
-__global__ void __launch_bounds__(kClThreads) cl_window_kernel(const __grid_constant__ ClosedArgs a) {
+__global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(const __grid_constant__ ClosedArgs a) {
     extern __shared__ uint32_t dyn[];                        // ring [N][W], then scratch [N][W]
     __shared__ unsigned long long wsum[N][NCM][2];          // window: requests, tokens per (level, class)
     __shared__ int head[N], size[N];
