@@ -105,8 +105,16 @@ __global__ void __launch_bounds__(kRedThreads) reduce_stage2(const __grid_consta
     const int64_t r = blockIdx.y;
     double v = 0.0;
     if (jk < per_row && r >= a.r_lo && r < a.r_hi) {
+        // only the chunks holding intervals of the shard: the others' partials are exact
+        // zeros (stage 1 skips foreign intervals), so the sum is the same bit for bit
+        const int64_t t_lo = max((int64_t)0, a.first_segment - r * a.T);
+        const int64_t t_hi = min(a.T, a.first_segment + a.n_segments - r * a.T);
+        const int c_lo = (int)(t_lo / a.chunk), c_hi = (int)((t_hi + a.chunk - 1) / a.chunk);
         const double *p = a.partials + (size_t)(r - a.r_lo) * a.n_chunks * per_row + jk;
-        for (int c = warp; c < a.n_chunks; c += kRedThreads / 32) v += p[(size_t)c * per_row];
+        int c = c_lo + warp;
+        // two accumulators interleaved would change the order; keep one, with the loads unrolled ahead
+#pragma unroll 8
+        for (; c < c_hi; c += kRedThreads / 32) v += p[(size_t)c * per_row];
     }
     part[warp][lane] = v;
     __syncthreads();
