@@ -332,6 +332,9 @@ def run_sprout(args):
         step()
     torch.cuda.synchronize()
     graph = None
+    # one GPU, the Sprout step: CUDA-graph replay by default (--no-graph for eager launches)
+    if args.graph is None:
+        args.graph = world == 1 and scheme == S.SCHEME_SPROUT and not args.closed_loop and not oracle_scheme
     if args.graph:   # the whole step (all its launches + the all-reduce) as one CUDA graph replay
         graph = sw.capture(step)
         for _ in range(args.warmup):
@@ -562,8 +565,10 @@ def main():
     ap.add_argument("--static-xi", type=float, default=0.1, help="xi of the Sprout_Sta quality floor")
     ap.add_argument("--closed-loop", type=int, default=0, metavar="W",
                     help="closed-loop profiles (NEXT-1): window of W requests per level; 0 = open loop")
-    ap.add_argument("--graph", action="store_true",
-                    help="replay the step as one captured CUDA graph (runner.Sweep.capture)")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=None,
+                    help="replay the step as one captured CUDA graph (runner.Sweep.capture); "
+                         "the default on one GPU for the Sprout step")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches")
     ap.add_argument("--q-update", action="store_true",
                     help="with --closed-loop: q updated per evaluation epoch (NEXT-1, reading L24) inside each step")
     ap.add_argument("--preference", action="store_true",
