@@ -2384,7 +2384,7 @@ static cudaError_t launch_n(SimArgs &a, const SimPlan &plan, cudaStream_t stream
                   : a.flags ? launch_trace_t<N, true>(a, plan, stream) : launch_trace_t<N, false>(a, plan, stream);
     if (e != cudaSuccess) return e;
     ++*launches;
-    if (a.levels_out) {
+    if (a.levels_out && !x1) {   // (the one-cell kernels write their requests' levels themselves)
         int64_t blocks = (a.n_segments * 32 + 255) / 256;
         if (blocks > 148 * 32) blocks = 148 * 32;
         levels_kernel<N><<<(unsigned)blocks, 256, 0, stream>>>(a);
@@ -2444,7 +2444,7 @@ cudaError_t launch_simulate(SimArgs &a, const SimPlan &plan, void *ws, cudaStrea
     // prep (also resets the queue and trace_status).  The one-cell kernels need no
     // breakpoints and check the offsets themselves: without verify mode they only
     // need the two counters reset
-    if (!kDisableX1 && trace_x1_supported(plan.n, a.X, a.NC) && !a.levels_out) {
+    if (!kDisableX1 && trace_x1_supported(plan.n, a.X, a.NC)) {
         cudaError_t e = cudaMemsetAsync(a.queue, 0, 4, stream);
         if (e == cudaSuccess) e = cudaMemsetAsync(a.trace_status, 0, 4, stream);
         if (e != cudaSuccess) return e;

@@ -25,7 +25,7 @@ constexpr int kX1Warps = 8;                   // warps per CTA
 constexpr bool kX1NoGroups = SPROUT_X1_NO_GROUPS;
 constexpr int64_t kX1Chunk = (int64_t)1 << 21; // requests per fold: <= 2^16 per lane, token sums <= 2^16 * 65535 < 2^32
 
-template <int N, bool FLAGS, bool NC2>
+template <int N, bool FLAGS, bool NC2, bool VB>
 #ifndef SPROUT_X1_MIN_BLOCKS
 #define SPROUT_X1_MIN_BLOCKS 3
 #endif
@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(32 * kX1Warps, SPROUT_X1_MIN_BLOCKS) trace_x1_
                     for (int i = 0; i + 1 < N; ++i) L += (w >= T[i]) ? 1 : 0;
                     L = min(L, ml);
                     L = pin ? 0 : L;
+                    if (VB && inr) a.levels_out[r] = (ok && cell_ok) ? (uint8_t)L : (uint8_t)0xFF;   // verify mode
                     uint32_t t[N], tL = 0u;
 #pragma unroll
                     for (int i = 0; i < N; ++i) {
@@ -221,7 +222,7 @@ __global__ void __launch_bounds__(32 * kX1Warps, SPROUT_X1_MIN_BLOCKS) trace_x1_
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(a.tokens + (size_t)i * a.pitch + rp));
                 }
             };
-            if (!FLAGS && !NC2 && pure) {
+            if (!FLAGS && !NC2 && pure && !VB) {
                 // pure mix, no flags: every request is at the same level -- a streaming sum of the
                 // token planes (interior quads whole, the two edge quads per request)
                 int Lp = 0;
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(32 * kX1Warps, SPROUT_X1_MIN_BLOCKS) trace_x1_
 // -- is shared by G segments, and a segment's quads keep 32/G lanes busy
 // instead of leaving most of 32 idle.  Outputs, formulas and order as
 // trace_x1_kernel.
-template <int N, bool FLAGS, bool NC2, int G>
+template <int N, bool FLAGS, bool NC2, int G, bool VB>
 __global__ void __launch_bounds__(32 * kX1Warps, SPROUT_X1_MIN_BLOCKS) trace_x1g_kernel(const __grid_constant__ SimArgs a) {
     constexpr int LG = 32 / G;                       // lanes per segment
     constexpr int NCc = NC2 ? 2 : 1;
@@ -481,6 +482,7 @@ __global__ void __launch_bounds__(32 * kX1Warps, SPROUT_X1_MIN_BLOCKS) trace_x1g
                         for (int i = 0; i + 1 < N; ++i) L += (w >= T[i]) ? 1 : 0;
                         L = min(L, ml);
                         L = pin ? 0 : L;
+                        if (VB && inr) a.levels_out[r] = (ok && cell_ok) ? (uint8_t)L : (uint8_t)0xFF;   // verify mode
                         uint32_t t[N], tL = 0u;
 #pragma unroll
                         for (int i = 0; i < N; ++i) {
@@ -597,7 +599,7 @@ __global__ void __launch_bounds__(32 * kX1Warps, SPROUT_X1_MIN_BLOCKS) trace_x1g
 
 template <int N, bool FLAGS, bool NC2, int G>
 static cudaError_t launch_x1g_t(SimArgs &a, cudaStream_t stream) {
-    auto kern = trace_x1g_kernel<N, FLAGS, NC2, G>;
+    auto kern = a.levels_out ? trace_x1g_kernel<N, FLAGS, NC2, G, true> : trace_x1g_kernel<N, FLAGS, NC2, G, false>;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -616,7 +618,7 @@ static cudaError_t launch_x1g_t(SimArgs &a, cudaStream_t stream) {
 
 template <int N, bool FLAGS, bool NC2>
 static cudaError_t launch_x1_t(SimArgs &a, cudaStream_t stream) {
-    auto kern = trace_x1_kernel<N, FLAGS, NC2>;
+    auto kern = a.levels_out ? trace_x1_kernel<N, FLAGS, NC2, true> : trace_x1_kernel<N, FLAGS, NC2, false>;
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
