@@ -386,6 +386,24 @@ def run_sprout(args):
     status = int(sw.totals.trace_status.item())
     g = sw.group.cpu().numpy()
 
+    # cross-check after the timed steps: the fp64 per-request accounting mode (Eq. 1 per
+    # request, fp64 warp-shuffle / block tree sums) against the streaming kernel's closed
+    # form, every cell of the full workload (sprout_cell_totals_fp64)
+    fp64_check = {}
+    if args.fp64_check and scheme == S.SCHEME_SPROUT and not args.closed_loop and not oracle_scheme:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        f64 = S.cell_totals_fp64(sw.dp, sw.sol, sw.trace, sw.cost)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = sw.totals
+        diffs = {}
+        for k, ref in (("energy", t.energy), ("time", t.time), ("carbon", t.carbon), ("quality", t.quality)):
+            den = torch.clamp(ref.abs(), min=1e-300)
+            diffs[k] = float(((f64[k] - ref).abs() / den).max().item()) if ref.numel() else 0.0
+        fp64_check = {"fp64_per_request_max_rel_diff": max(diffs.values()) if diffs else 0.0,
+                      "fp64_per_request_ms": e0.elapsed_time(e1)}
+
     # NEXT-4 reporting (untimed by the step; each kernel timed on its own)
     extras = {}
     if args.preference and not args.closed_loop:
@@ -483,7 +501,8 @@ def run_sprout(args):
         "trace_status": status,
         **extras,
         "check": {"requests_counted": float(g[-1, 0, 0]),
-                  "carbon_saving_xi_max": float(1 - g[-1, -1, 4] / g[-1, -1, 8]) if g[-1, -1, 8] > 0 else None},
+                  "carbon_saving_xi_max": float(1 - g[-1, -1, 4] / g[-1, -1, 8]) if g[-1, -1, 8] > 0 else None,
+                  **fp64_check},
     }
     print(json.dumps(line))
     if world > 1:
@@ -569,6 +588,8 @@ def main():
                     help="replay the step as one captured CUDA graph (runner.Sweep.capture); "
                          "the default on one GPU for the Sprout step")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="eager launches")
+    ap.add_argument("--no-fp64-check", dest="fp64_check", action="store_false",
+                    help="skip the after-the-run fp64 per-request cross-check of every cell")
     ap.add_argument("--q-update", action="store_true",
                     help="with --closed-loop: q updated per evaluation epoch (NEXT-1, reading L24) inside each step")
     ap.add_argument("--preference", action="store_true",
