@@ -283,10 +283,18 @@ def run_sprout(args):
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
 
+    # SPROUT_BENCH_SHARE_GPU=1 (functional test of the N > 1 path on a one-GPU box only: every
+    # rank on device local % count, gloo; its timings are not a measurement)
+    share = os.environ.get("SPROUT_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     w = scheme_workload(args)
     scheme = SCHEMES[args.scheme]
@@ -441,25 +449,26 @@ def run_sprout(args):
     if not args.no_e2e and scheme == S.SCHEME_SPROUT and not args.closed_loop:
         e2e = run_e2e(args, w, sh, sw, dev, world)
 
+    # the roofline's bytes and time over the job (collectives: every rank, before rank 0 reports):
+    # per-GPU average = all ranks' algorithmic bytes over the slowest rank's simulate time
+    alg = algorithmic_bytes(w, sh)
+    if args.closed_loop:   # the trace once (the chains of a region share it) + every interval's LP outputs
+        P = w.prob
+        alg = algorithmic_bytes(w, sh) + sh.n_segments * P.X * (P.n * 8 + 8 + 8)
+    sim_job_ms = (statistics.mean(sim_ms), statistics.median(sim_ms))
+    if world > 1:
+        t = torch.tensor([float(alg)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        alg = float(t.item()) / world
+        sim_job_ms = (max_over_ranks(sim_job_ms[0], dev), max_over_ranks(sim_job_ms[1], dev))
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
     peak, peak_src = peaks()
-    alg = algorithmic_bytes(w, sh)
-    if args.closed_loop:   # the trace once (the chains of a region share it) + every interval's LP outputs
-        P = w.prob
-        f = 1 if w.spec.has_flags else 0
-        alg = algorithmic_bytes(w, sh) + sh.n_segments * P.X * (P.n * 8 + 8 + 8)
-    sim_avg_ms = statistics.mean(sim_ms)
-    sim_med_ms = statistics.median(sim_ms)
-    if world > 1:   # per-GPU average over the job: all ranks' bytes over the slowest rank's time
-        t = torch.tensor([float(alg)], dtype=torch.float64, device=dev)
-        dist.all_reduce(t)
-        alg = float(t.item()) / world
-        sim_avg_ms = max_over_ranks(sim_avg_ms, dev)
-        sim_med_ms = max_over_ranks(sim_med_ms, dev)
+    sim_avg_ms, sim_med_ms = sim_job_ms
     achieved = alg / (sim_avg_ms * 1e-3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
