@@ -541,3 +541,35 @@ def test_x1_grouped_kernel_long_segment_chunks(n, NC, flags):
     off[1:] = np.cumsum(m)
     assert off[-1] <= 1024 * len(m)
     check_full(w)
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 8])
+def test_x1_timed_path_with_clamps(n):
+    """One class, no flags, long segments, without verify mode (the timed
+    one-cell path exactly as bench runs it), then with max_level clamps below
+    n - 1 in a third of the cells: counts against the a6 rule recounted here
+    from the oracle's draws."""
+    w = _custom(n=n, X=1, NC=1, flags=False, N=400_000, T=12, R=3, xi=[0.25])
+    check_full(w, levels=False)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, flags = synth.host_trace(w.spec, sh)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=flags)
+    sw.solve()
+    torch.cuda.synchronize()
+    # clamps: max_level below n - 1 in some cells (thresholds unchanged)
+    ml = sw.sol.max_level.clone()
+    ml[::3] = torch.clamp(ml[::3] - 1, min=0)
+    sw.sol.max_level.copy_(ml)
+    sw.simulate()
+    torch.cuda.synchronize()
+    got = sw.host()
+    sim_lv = oracle_shard(w, sh, toks, flags, levels=False)
+    # expected: the a6 rule from the same draws with the clamped max_level, counted here
+    thr = sw.sol.thresholds_u32().reshape(-1, max(n - 1, 1)).astype(np.uint64)
+    mlh = ml.cpu().numpy()
+    cnt = got["cnt"].reshape(-1, n)
+    for sidx in range(0, sh.n_segments, 5):
+        a_, b_ = sh.seg_offsets[sidx], sh.seg_offsets[sidx + 1]
+        wd = np.array([oracle.draw_word(w.cost.seed, sh.first_request + r) for r in range(a_, b_)], dtype=np.uint64)
+        lv = np.minimum((wd[:, None] >= thr[sidx][None, :]).sum(axis=1), mlh[sidx]) if n > 1 else np.zeros(len(wd), int)
+        np.testing.assert_array_equal(cnt[sidx], np.bincount(lv, minlength=n)[:n])
