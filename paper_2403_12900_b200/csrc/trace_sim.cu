@@ -53,6 +53,9 @@ constexpr int kMaxTraceWarps = SPROUT_TRACE_WARPS;
 #ifndef SPROUT_DISABLE_X1
 #define SPROUT_DISABLE_X1 0
 #endif
+#ifndef SPROUT_RMW_QUAD
+#define SPROUT_RMW_QUAD 0   // A/B: read-modify-write four requests per link instead of two
+#endif
 constexpr bool kDisableX1 = SPROUT_DISABLE_X1;   // A/B only: route X = 1 through the general kernel
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
@@ -663,6 +666,38 @@ __device__ __forceinline__ void rmw_pair(const Group<N, FLAGS> &g, int k, uint32
     }
 }
 
+// Read-modify-write of the rows of requests k..k+3 (k % 4 == 0): the four loads
+// issue together, the increments are folded in registers in request order
+// (a later request hitting an earlier one's row starts from that request's
+// updated value), and the stores stay in request order, so the last store to
+// a row carries every increment.  Half the dependent links of rmw_pair.
+template <int N, bool FLAGS>
+__device__ __forceinline__ void rmw_quad(const Group<N, FLAGS> &g, int k, uint32_t r0, uint32_t r1, uint32_t r2,
+                                         uint32_t r3, uint32_t &acc0, uint32_t &acc) {
+    constexpr int NP = Words<N>::NP;
+    const bool e10 = r1 == r0, e20 = r2 == r0, e21 = r2 == r1, e30 = r3 == r0, e31 = r3 == r1, e32 = r3 == r2;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        uint2 A0 = lds64(r0 + p * 256);
+        const uint2 L1 = lds64(r1 + p * 256), L2 = lds64(r2 + p * 256), L3 = lds64(r3 + p * 256);
+        const uint2 i0 = packed_inc<N, FLAGS>(g, k, p), i1 = packed_inc<N, FLAGS>(g, k + 1, p);
+        const uint2 i2 = packed_inc<N, FLAGS>(g, k + 2, p), i3 = packed_inc<N, FLAGS>(g, k + 3, p);
+        A0.x += i0.x; A0.y += i0.y;
+        uint2 A1 = e10 ? A0 : L1;
+        A1.x += i1.x; A1.y += i1.y;
+        uint2 A2 = e21 ? A1 : (e20 ? A0 : L2);
+        A2.x += i2.x; A2.y += i2.y;
+        uint2 A3 = e32 ? A2 : (e31 ? A1 : (e30 ? A0 : L3));
+        A3.x += i3.x; A3.y += i3.y;
+        sts64(r0 + p * 256, A0);
+        sts64(r1 + p * 256, A1);
+        sts64(r2 + p * 256, A2);
+        sts64(r3 + p * 256, A3);
+        if (p == 0) { acc0 |= A0.x | A1.x | A2.x | A3.x; acc |= A0.y | A1.y | A2.y | A3.y; }
+        else { acc |= A0.x | A0.y | A1.x | A1.y | A2.x | A2.y | A3.x | A3.y; }
+    }
+}
+
 // The read-modify-write chain of a group (a request's load may alias an
 // earlier request's store, so updates are serialised through shared memory,
 // two requests per link) interleaved, in program order, with the
@@ -693,6 +728,13 @@ __device__ __forceinline__ uint32_t update_fast(const Group<N, FLAGS> &g, const 
                 on.v[k + 4] = lut_offset(wn.v[k + 4], geo, rowbytes, lane_base, en);
                 on.v[k + 5] = lut_offset(wn.v[k + 5], geo, rowbytes, lane_base, en);
             }
+        }
+#elif SPROUT_RMW_QUAD
+#pragma unroll
+        for (int k = 0; k < 8; k += 4) {
+            rmw_quad<N, FLAGS>(g, k, row.v[k], row.v[k + 1], row.v[k + 2], row.v[k + 3], acc0, acc);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) on.v[k + u] = lut_offset(wn.v[k + u], geo, rowbytes, lane_base, en);
         }
 #else
 #pragma unroll
