@@ -267,9 +267,17 @@ size_t oracle_scheme_workspace_bytes(int64_t cap) {
     return 256 + (size_t)sms * or_cta_bytes(cap);
 }
 
+// radix digits of the candidates' 64-bit keys: 11 bits (six passes over the key,
+// those with a single digit value skipped); per-warp digit histograms in dynamic
+// shared memory ([kOrWarps][kOrDigits] u32, 128 KB)
+constexpr int kOrBits = 11;
+constexpr int kOrDigits = 1 << kOrBits;
+constexpr size_t kOrDynSmem = (size_t)kOrWarps * kOrDigits * 4;
+
 struct OrSmem {
-    uint32_t hist[kOrWarps][256];
-    uint32_t dtot[256];
+    uint32_t hist[kOrWarps][256];   // pass 1: per-warp candidate counts
+    uint32_t dtot[kOrDigits];       // the sort: per-digit totals, then exclusive digit offsets
+    uint32_t wsum[kOrWarps];
     int64_t seg;
     int skip;
 };
@@ -277,6 +285,7 @@ struct OrSmem {
 template <int N, int NCM>
 __global__ void __launch_bounds__(kOrThreads) oracle_scheme_kernel(const __grid_constant__ N4Args a) {
     __shared__ OrSmem sm;
+    extern __shared__ uint32_t hdyn[];   // [kOrWarps][kOrDigits]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t cap = a.cap;
     uint8_t *scr = a.scratch + (size_t)blockIdx.x * or_cta_bytes(cap);
@@ -438,37 +447,58 @@ __global__ void __launch_bounds__(kOrThreads) oracle_scheme_kernel(const __grid_
         }
         __syncthreads();
         const int64_t nc = (int64_t)ncand;
-        // ---- stable LSD radix sort of (key, index), 8 bits per pass ----
+        // ---- stable LSD radix sort of (key, index), kOrBits bits per pass ----
         unsigned long long *ks = keyA, *kd = keyB;
         uint32_t *is = idxA, *id = idxB;
         const int64_t per = (nc + kOrWarps - 1) / kOrWarps;   // warp w: [w*per, (w+1)*per)
         const int64_t lo = min(nc, (int64_t)warp * per), hi = min(nc, lo + per);
-        for (int pass = 0; pass < 8; ++pass) {
-            const int sh = 8 * pass;
-            for (int i = lane; i < 256; i += 32) sm.hist[warp][i] = 0u;
+        uint32_t *wh = hdyn + (size_t)warp * kOrDigits;      // this warp's digit histogram
+        for (int sh = 0; sh < 64; sh += kOrBits) {
+            const unsigned long long dmask = (unsigned long long)(kOrDigits - 1);
+            for (int i = lane; i < kOrDigits; i += 32) wh[i] = 0u;
             __syncwarp();
-            for (int64_t i = lo + lane; i < hi; i += 32) atomicAdd(&sm.hist[warp][(ks[i] >> sh) & 0xFFu], 1u);
+            for (int64_t i = lo + lane; i < hi; i += 32) atomicAdd(&wh[(ks[i] >> sh) & dmask], 1u);
             __syncthreads();
-            // skip the pass if one digit holds every key (thread d: digit d's total)
+            // per-digit totals; skip the pass if one digit holds every key
             if (tid == 0) sm.skip = 0;
-            if (tid < 256) {
+            for (int d = tid; d < kOrDigits; d += kOrThreads) {
                 uint32_t t = 0u;
-                for (int w2 = 0; w2 < kOrWarps; ++w2) t += sm.hist[w2][tid];
-                sm.dtot[tid] = t;
+                for (int w2 = 0; w2 < kOrWarps; ++w2) t += hdyn[(size_t)w2 * kOrDigits + d];
+                sm.dtot[d] = t;
             }
             __syncthreads();
-            if (tid < 256 && (int64_t)sm.dtot[tid] == nc) sm.skip = 1;
+            for (int d = tid; d < kOrDigits; d += kOrThreads)
+                if ((int64_t)sm.dtot[d] == nc) sm.skip = 1;
             __syncthreads();
             if (sm.skip) continue;
-            // exclusive offsets in (digit, warp) order: thread d over its digit's warps, after the
-            // digits before it
-            if (tid < 256) {
-                uint32_t before = 0u;
-                for (int d = 0; d < tid; ++d) before += sm.dtot[d];
-                for (int w2 = 0; w2 < kOrWarps; ++w2) {
-                    const uint32_t v = sm.hist[w2][tid];
-                    sm.hist[w2][tid] = before;
-                    before += v;
+            // exclusive offsets in (digit, warp) order: a block scan of the digit totals
+            // (thread t owns digits [t*D, (t+1)*D), D = kOrDigits / kOrThreads), then
+            // each digit's warps in order
+            {
+                constexpr int D = kOrDigits / kOrThreads;
+                uint32_t loc[D], run = 0u;
+#pragma unroll
+                for (int k = 0; k < D; ++k) { loc[k] = run; run += sm.dtot[tid * D + k]; }
+                uint32_t x = run;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, d);
+                    if (lane >= d) x += y;
+                }
+                if (lane == 31) sm.wsum[warp] = x;
+                __syncthreads();
+                uint32_t before = x - run;
+                for (int w2 = 0; w2 < warp; ++w2) before += sm.wsum[w2];
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const int dg = tid * D + k;
+                    uint32_t off = before + loc[k];
+                    for (int w2 = 0; w2 < kOrWarps; ++w2) {
+                        uint32_t *h = &hdyn[(size_t)w2 * kOrDigits + dg];
+                        const uint32_t v = *h;
+                        *h = off;
+                        off += v;
+                    }
                 }
             }
             __syncthreads();
@@ -477,16 +507,16 @@ __global__ void __launch_bounds__(kOrThreads) oracle_scheme_kernel(const __grid_
                 const int64_t i = i0 + lane;
                 const bool in = i < hi;
                 const unsigned long long kv = in ? ks[i] : 0ull;
-                const uint32_t dg = in ? (uint32_t)((kv >> sh) & 0xFFu) : 256u + (uint32_t)lane;
+                const uint32_t dg = in ? (uint32_t)((kv >> sh) & dmask) : (uint32_t)kOrDigits + (uint32_t)lane;
                 const uint32_t peers = __match_any_sync(0xFFFFFFFFu, dg);
                 if (in) {
                     const uint32_t rank = __popc(peers & ((1u << lane) - 1u));
-                    const uint32_t pos = sm.hist[warp][dg] + rank;
+                    const uint32_t pos = wh[dg] + rank;
                     kd[pos] = kv;
                     id[pos] = is[i];
                 }
                 __syncwarp();
-                if (in && (__ffs(peers) - 1) == lane) sm.hist[warp][dg] += __popc(peers);
+                if (in && (__ffs(peers) - 1) == lane) wh[dg] += __popc(peers);
                 __syncwarp();
             }
             __syncthreads();
@@ -625,10 +655,13 @@ cudaError_t launch_oracle_scheme(N4Args &a, cudaStream_t stream, int *launches) 
     int64_t grid = sm_count();
     if (grid > a.n_segments) grid = a.n_segments;
 #define OR_CASE(NN)                                                                                     \
-    case NN:                                                                                            \
-        if (a.NC > 1) oracle_scheme_kernel<NN, kMaxClasses><<<(unsigned)grid, kOrThreads, 0, stream>>>(a); \
-        else oracle_scheme_kernel<NN, 1><<<(unsigned)grid, kOrThreads, 0, stream>>>(a);                \
-        break;
+    case NN: {                                                                                          \
+        auto kern = a.NC > 1 ? oracle_scheme_kernel<NN, kMaxClasses> : oracle_scheme_kernel<NN, 1>;     \
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kOrDynSmem); \
+        if (e != cudaSuccess) return e;                                                                 \
+        kern<<<(unsigned)grid, kOrThreads, kOrDynSmem, stream>>>(a);                                    \
+        break;                                                                                          \
+    }
     switch (a.n) {
         OR_CASE(1) OR_CASE(2) OR_CASE(3) OR_CASE(4) OR_CASE(5) OR_CASE(6) OR_CASE(7) OR_CASE(8)
         default: return cudaErrorInvalidValue;
