@@ -63,12 +63,12 @@ struct Chunk {
     uint2 fw;
     uint32_t w[8];
 };
-template <int N>
+template <int N, bool FLAGS = true>
 __device__ __forceinline__ void load_chunk(const ClosedArgs &a, int64_t c0, bool any, Chunk<N> &ch) {
     if (any) {
 #pragma unroll
         for (int L = 0; L < N; ++L) ch.tk[L] = __ldcs(reinterpret_cast<const uint4 *>(a.tokens + (size_t)L * a.pitch + c0));
-        ch.fw = a.flags ? __ldcs(reinterpret_cast<const uint2 *>(a.flags + c0)) : make_uint2(0u, 0u);
+        ch.fw = (FLAGS && a.flags) ? __ldcs(reinterpret_cast<const uint2 *>(a.flags + c0)) : make_uint2(0u, 0u);
         const uint64_t blk = (a.first_request + (uint64_t)c0) >> 2;
         const Philox4 d0 = philox4x32_10_rk((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, a.rk0, a.rk1);
         const Philox4 d1 = philox4x32_10_rk((uint32_t)(blk + 1), (uint32_t)((blk + 1) >> 32), 0u, 0u, a.rk0, a.rk1);
@@ -116,7 +116,7 @@ __device__ __forceinline__ void prefetch_piece(const ClosedArgs &a, int64_t p0, 
 // segment totals are not accumulated here: once every interval's thresholds
 // are known they are exactly the open-loop totals of those thresholds, and
 // the caller (sprout_abi.cu) runs the streaming simulate kernel for them.
-template <int N, int NCM>
+template <int N, int NCM, bool FLAGS>
 __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(const __grid_constant__ ClosedArgs a) {
     extern __shared__ uint32_t dyn[];                        // ring [N][W], then scratch [N][W]
     __shared__ unsigned long long wsum[N][NCM][2];          // window: requests, tokens per (level, class)
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
         Chunk<N> ch;
         const int64_t c00 = e_al - kClPiece + 8 * (int64_t)tid;
         const bool any0 = s0 <= s1 && c00 + 8 > s0 && c00 < s1 && s1 <= a.n_requests && s0 >= 0;
-        if (warp != 0) load_chunk<N>(a, c00, any0, ch);
+        if (warp != 0) load_chunk<N, FLAGS>(a, c00, any0, ch);
         // ---- the interval's LP with the closed-loop profile ----
         if (tid == 0) {
             const int64_t cell = sl * a.X + j;
@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
             // levels the mix can reach (a6 is a step function of the draw with steps at the
             // thresholds, so evaluating it at 0, 2^32 - 1 and on both sides of every
             // threshold finds them all); opted-out requests reach L0
-            int act = a.flags ? 1 : 0;
+            int act = FLAGS ? 1 : 0;
             if (ok) {
                 act |= 1 << cl_level<N>(0u, o.T, o.max_level, false);
                 act |= 1 << cl_level<N>(0xFFFFFFFFu, o.T, o.max_level, false);
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
         const int ml = ml_s;
         // ---- backward scan: the interval's last W requests of every reachable level ----
         if (run) {
-            if (warp == 0) load_chunk<N>(a, c00, any0, ch);
+            if (warp == 0) load_chunk<N, FLAGS>(a, c00, any0, ch);
             const int64_t b_al = s0 & ~(int64_t)7;
             const int n_pieces = (int)((e_al - b_al + kClPiece - 1) / kClPiece);
             uint32_t seen_r = 0u;   // lane L < N: level-L requests scanned so far (every warp the same)
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
                 const int64_t base = e_al - (int64_t)(pi + 1) * kClPiece;
                 prefetch_piece<N>(a, base - 2 * (int64_t)kClPiece, s1, tid);
                 const int64_t c0 = base + 8 * (int64_t)tid;
-                if (pi > 0) load_chunk<N>(a, c0, c0 + 8 > s0 && c0 < s1, ch);
+                if (pi > 0) load_chunk<N, FLAGS>(a, c0, c0 + 8 > s0 && c0 < s1, ch);
                 // valid requests of the chunk: inside [s0, s1) (a bit range) with a class < NC
                 uint32_t valid;
                 {
@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
                     const uint32_t fb = flag_byte(ch.fw, k);
-                    if (a.flags && ((fb >> 1) & 3u) >= (uint32_t)NC) valid &= ~(1u << k);
-                    const int L = cl_level<N>(ch.w[k], T, ml, fb & 1u);
+                    if (FLAGS && ((fb >> 1) & 3u) >= (uint32_t)NC) valid &= ~(1u << k);
+                    const int L = cl_level<N>(ch.w[k], T, ml, FLAGS && (fb & 1u));
                     lv |= (uint32_t)L << (4 * k);
                     pk += ((valid >> k) & 1u) ? (1ull << (8 * L)) : 0ull;
                 }
@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
 #pragma unroll
                         for (int LL = 0; LL < N; ++LL)
                             if (LL == L) { rho = after[LL]; after[LL] += 1u; tl = cl_half(ch.tk[LL], k); }
-                        if (rho < (uint32_t)W) scr[(size_t)L * W + rho] = (((flag_byte(ch.fw, k) >> 1) & 3u) << 16) | tl;
+                        if (rho < (uint32_t)W)
+                            scr[(size_t)L * W + rho] = (FLAGS ? (((flag_byte(ch.fw, k) >> 1) & 3u) << 16) : 0u) | tl;
                     }
                 }
                 if (done) break;
@@ -399,7 +400,7 @@ cudaError_t launch_closed_loop(ClosedArgs &a, cudaStream_t stream, int *launches
     cudaError_t e = cudaSuccess;
 #define CL_LAUNCH(NN, NCM_)                                                                       \
     {                                                                                             \
-        auto kern = cl_window_kernel<NN, NCM_>;                                                   \
+        auto kern = a.flags ? cl_window_kernel<NN, NCM_, true> : cl_window_kernel<NN, NCM_, false>; \
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
         if (e != cudaSuccess) return e;                                                           \
         kern<<<(unsigned)blocks, kClThreads, smem, stream>>>(a);                                  \
