@@ -163,11 +163,13 @@ def test_evaluation_q_and_closed_loop_q(name, kw, dt, grace, sample):
     np.testing.assert_allclose(got["carbon"].reshape(-1), want["carbon"], rtol=FP_RTOL, atol=0)
 
 
-@pytest.mark.parametrize("n,NC,flags,W", [(1, 1, False, 3), (8, 1, False, 40), (4, 4, True, 25), (2, 3, True, 1)])
+@pytest.mark.parametrize("n,NC,flags,W", [(1, 1, False, 3), (8, 1, False, 40), (4, 4, True, 25), (2, 3, True, 1),
+                                            (3, 1, True, 25), (2, 1, False, 2000), (4, 1, True, 700)])
 def test_closed_loop_levels_classes_ragged(n, NC, flags, W):
     """The chain kernel's other template instances (n = 1, n = 8, four
-    classes) on ragged intervals: empty ones, single requests, and one longer
-    than several scan pieces."""
+    classes; two xi chains per CTA with and without flags, X = 3 leaving the
+    last group one chain short) on ragged intervals: empty ones, single
+    requests, and one longer than several scan pieces."""
     from test_gpu_parity import _custom
     w = _custom(n=n, X=3, NC=NC, flags=flags, N=30_000, T=30, R=2, xi=[0.0, 0.35, 1.0])
     off = w.spec.seg_offsets
