@@ -7,6 +7,13 @@
 // (lp_cell.cuh, the same arithmetic as step 1), and the interval's requests
 // are replayed and pushed into their level's window.
 //
+// Chains cost very different times (an interval is scanned back until every
+// level its mix reaches has W requests, so a level with a small share makes
+// the scan deep): two small kernels first estimate each chain's scan work
+// from the LP on the priors and order the chains longest first, so a long
+// chain does not start last.  A chain gets 512 threads (one CTA per SM) when
+// the intervals are long, 256 otherwise.
+//
 // A chain is sequential in time by definition, but only the LP decisions and
 // the windows are: once every interval's thresholds are known, the cell
 // totals are exactly the open-loop totals of those thresholds.  So the chain
@@ -22,6 +29,7 @@
 // order exactly.  With E = ef + et*tok (reading L11) the window mean is a
 // function of per-class counts and token sums -- exact integers -- so the
 // profile, and the LP decision it feeds, are bit-identical to the oracle's.
+#include <cstdio>
 #include <cuda_runtime.h>
 #include "sprout_device.cuh"
 #include "sprout_kernels.cuh"
@@ -29,15 +37,14 @@
 
 namespace sprout {
 
-#ifndef SPROUT_CL_THREADS
-#define SPROUT_CL_THREADS 256
+#ifndef SPROUT_CL_TIMING_NO_MEM
+#define SPROUT_CL_TIMING_NO_MEM 0
 #endif
-#ifndef SPROUT_CL_MINB
-#define SPROUT_CL_MINB 2
-#endif
-constexpr int kClThreads = SPROUT_CL_THREADS;
-constexpr int kClWarps = kClThreads / 32;
-constexpr int kClPiece = 8 * kClThreads;   // requests per piece: 8 per thread
+// threads per chain: 512 (one CTA per SM) when the intervals are long enough
+// that fewer, larger scan pieces pay; 256 (two per SM) for short intervals,
+// where a piece covers the whole interval and a 16-warp barrier only costs
+constexpr int kClThreadsLong = 512, kClThreadsShort = 256;
+constexpr int64_t kClLongInterval = 2 * 8 * kClThreadsShort;   // mean requests per interval for 512
 
 __device__ __forceinline__ uint32_t cl_half(uint4 u, int k) {   // u16 token k of a 16-byte group
     const uint32_t w = (k >> 1) == 0 ? u.x : (k >> 1) == 1 ? u.y : (k >> 1) == 2 ? u.z : u.w;
@@ -67,13 +74,22 @@ template <int N, bool FLAGS = true>
 __device__ __forceinline__ void load_chunk(const ClosedArgs &a, int64_t c0, bool any, Chunk<N> &ch) {
     if (any) {
 #pragma unroll
+#if SPROUT_CL_TIMING_NO_MEM   // timing-only A/B: every chunk from one 2 KB window (cache hits)
+        for (int L = 0; L < N; ++L) ch.tk[L] = __ldca(reinterpret_cast<const uint4 *>(a.tokens + (size_t)L * a.pitch + (c0 & 1023)));
+#else
         for (int L = 0; L < N; ++L) ch.tk[L] = __ldcs(reinterpret_cast<const uint4 *>(a.tokens + (size_t)L * a.pitch + c0));
+#endif
         ch.fw = (FLAGS && a.flags) ? __ldcs(reinterpret_cast<const uint2 *>(a.flags + c0)) : make_uint2(0u, 0u);
         const uint64_t blk = (a.first_request + (uint64_t)c0) >> 2;
+#if SPROUT_CL_TIMING_NO_PHILOX   // timing-only A/B: a cheap hash instead of the draws (wrong levels)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ch.w[k] = ((uint32_t)blk + 0x9E3779B9u * (uint32_t)(k + 1)) * 0x85EBCA6Bu;
+#else
         const Philox4 d0 = philox4x32_10_rk((uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u, a.rk0, a.rk1);
         const Philox4 d1 = philox4x32_10_rk((uint32_t)(blk + 1), (uint32_t)((blk + 1) >> 32), 0u, 0u, a.rk0, a.rk1);
 #pragma unroll
         for (int k = 0; k < 4; ++k) { ch.w[k] = d0.v[k]; ch.w[4 + k] = d1.v[k]; }
+#endif
     } else {
 #pragma unroll
         for (int L = 0; L < N; ++L) ch.tk[L] = make_uint4(0u, 0u, 0u, 0u);
@@ -86,10 +102,10 @@ __device__ __forceinline__ uint32_t flag_byte(uint2 fw, int k) { return ((k < 4 
 
 // L2 prefetch of the piece starting at local request p0 (up to s1): one 128-byte
 // line per thread, 32 lines per token plane and 16 of flags
-template <int N>
+template <int N, int TH>
 __device__ __forceinline__ void prefetch_piece(const ClosedArgs &a, int64_t p0, int64_t s1, int tid) {
-    constexpr int kLines = kClPiece * 2 / 128;   // 32 lines of one token plane
-    if (p0 >= s1) return;
+    constexpr int kLines = 8 * TH * 2 / 128;   // the lines of one token plane of a piece
+    if (SPROUT_CL_TIMING_NO_MEM || p0 >= s1) return;
     if (tid < kLines * N) {
         const int q = tid / kLines, l = tid % kLines;
         const int64_t r = p0 + 64 * (int64_t)l;
@@ -104,7 +120,7 @@ __device__ __forceinline__ void prefetch_piece(const ClosedArgs &a, int64_t p0, 
 // Per interval: thread 0 forms the profile from the window sums and solves
 // the LP (lp_cell.cuh; the solution arrays receive x, thresholds, ...);
 // then the interval is scanned BACKWARDS from its end in pieces of
-// kClPiece requests (8 per thread: one 128-bit load per token plane, two
+// 8 * threads requests (8 per thread: one 128-bit load per token plane, two
 // Philox calls), each request's level found with the interval's thresholds,
 // and its reverse rank among the interval's level-L requests (a block-wide
 // suffix scan of per-thread counts) decides whether it is among the last W:
@@ -116,8 +132,9 @@ __device__ __forceinline__ void prefetch_piece(const ClosedArgs &a, int64_t p0, 
 // segment totals are not accumulated here: once every interval's thresholds
 // are known they are exactly the open-loop totals of those thresholds, and
 // the caller (sprout_abi.cu) runs the streaming simulate kernel for them.
-template <int N, int NCM, bool FLAGS>
-__global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(const __grid_constant__ ClosedArgs a) {
+template <int N, int NCM, bool FLAGS, int TH>
+__global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 2) cl_window_kernel(const __grid_constant__ ClosedArgs a) {
+    constexpr int kClThreads = TH, kClWarps = TH / 32, kClPiece = 8 * TH;   // a piece: 8 requests per thread
     extern __shared__ uint32_t dyn[];                        // ring [N][W], then scratch [N][W]
     __shared__ unsigned long long wsum[N][NCM][2];          // window: requests, tokens per (level, class)
     __shared__ int head[N], size[N];
@@ -129,7 +146,12 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
     const int W = a.W, NC = a.NC;
     uint32_t *ring = dyn, *scr = dyn + (size_t)N * W;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rl = blockIdx.x / a.X, j = blockIdx.x % a.X;
+    const int chain = a.chain_order ? a.chain_order[blockIdx.x] : (int)blockIdx.x;   // longest first
+    const int rl = chain / a.X, j = chain % a.X;
+#if SPROUT_CL_TIMING_PRINT
+    unsigned long long t_start;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
     const int r = a.r0 + rl;                                 // global region
     const CostConst &cost = a.cost;
     if (tid < N) { head[tid] = 0; size[tid] = 0; }
@@ -147,6 +169,9 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
     double nq[N];
 #pragma unroll
     for (int L = 0; L < N; ++L) nq[L] = (tid == 0 && a.q_seg) ? a.q_seg[(int64_t)r * a.T * N + L] : 0.0;
+#if SPROUT_CL_TIMING_NO_LP
+    LpCell<N> o_keep;
+#endif
     __syncthreads();
     for (int64_t t = 0; t < a.T; ++t) {
         const int64_t s = (int64_t)r * a.T + t;          // global segment (k0, profiles)
@@ -205,7 +230,12 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
                 }
             }
             LpCell<N> o;
+#if SPROUT_CL_TIMING_NO_LP   // timing-only A/B: the first interval's LP reused
+            if (t == 0) lp_cell<N>(k0_s, kmin_r, kmax_r, xi_j, e, p, q, a.k1, a.pue, 0, 0, j, o_keep);
+            o = o_keep;
+#else
             lp_cell<N>(k0_s, kmin_r, kmax_r, xi_j, e, p, q, a.k1, a.pue, 0, 0, j, o);
+#endif
 #pragma unroll
             for (int i = 0; i < N; ++i) a.x[cell * N + i] = o.x[i];
             a.objective[cell] = o.objective;
@@ -249,7 +279,7 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
             uint32_t seen_r = 0u;   // lane L < N: level-L requests scanned so far (every warp the same)
             for (int pi = 0; pi < n_pieces; ++pi) {
                 const int64_t base = e_al - (int64_t)(pi + 1) * kClPiece;
-                prefetch_piece<N>(a, base - 2 * (int64_t)kClPiece, s1, tid);
+                prefetch_piece<N, TH>(a, base - 2 * (int64_t)kClPiece, s1, tid);
                 const int64_t c0 = base + 8 * (int64_t)tid;
                 if (pi > 0) load_chunk<N, FLAGS>(a, c0, c0 + 8 > s0 && c0 < s1, ch);
                 // valid requests of the chunk: inside [s0, s1) (a bit range) with a class < NC
@@ -357,8 +387,8 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
             const int64_t n0 = a.seg_offsets[sl + 1], n1 = a.seg_offsets[sl + 2];
             if (n0 >= 0 && n0 <= n1 && n1 <= a.n_requests) {
                 const int64_t e2 = (n1 + 7) & ~(int64_t)7;
-                prefetch_piece<N>(a, e2 - kClPiece, n1, tid);
-                prefetch_piece<N>(a, e2 - 2 * kClPiece, n1, tid);
+                prefetch_piece<N, TH>(a, e2 - kClPiece, n1, tid);
+                prefetch_piece<N, TH>(a, e2 - 2 * kClPiece, n1, tid);
             }
         }
         {
@@ -390,20 +420,107 @@ __global__ void __launch_bounds__(kClThreads, SPROUT_CL_MINB) cl_window_kernel(c
         }
         __syncthreads();
     }
+#if SPROUT_CL_TIMING_PRINT
+    if (tid == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        printf("CHAIN %d %d %d %.3f %.3f\n", (int)blockIdx.x, rl, j, t_start * 1e-6, (t_end - t_start) * 1e-6);
+    }
+#endif
 }
+
+// Scheduling only (no result depends on it).  A chain's run time is its
+// intervals' scan depths, and those vary a lot between chains: an interval
+// is scanned back until each level the mix reaches has W requests, so a
+// level the mix gives a small fraction x_L needs W / x_L requests, up to the
+// whole interval.  The estimate solves each interval's LP with the priors
+// (the open-loop decision; the closed-loop profiles move it, the depth order
+// of the chains much less) and counts pieces; the chains then launch longest
+// first, so the long ones do not start last behind a wave of short ones.
+template <int N>
+__global__ void __launch_bounds__(256) cl_estimate_kernel(const __grid_constant__ ClosedArgs a, int piece) {
+    __shared__ float red[8];
+    const int c = blockIdx.x, rl = c / a.X, j = c % a.X, r = a.r0 + rl;
+    double e[N], p[N], qc[N];
+#pragma unroll
+    for (int L = 0; L < N; ++L) { e[L] = a.e[(int64_t)r * N + L]; p[L] = a.p[(int64_t)r * N + L]; qc[L] = a.q[(int64_t)r * N + L]; }
+    const double kmin = a.kmin[r], kmax = a.kmax[r], xi = a.xi[j];
+    float acc = 0.0f;
+    for (int64_t t = threadIdx.x; t < a.T; t += blockDim.x) {
+        const int64_t s = (int64_t)r * a.T + t, sl = s - a.first_segment;
+        double q[N];
+#pragma unroll
+        for (int L = 0; L < N; ++L) q[L] = a.q_seg ? a.q_seg[s * N + L] : qc[L];
+        LpCell<N> o;
+        lp_cell<N>(a.k0[s], kmin, kmax, xi, e, p, q, a.k1, a.pue, 0, 0, j, o);
+        const double m = (double)max(a.seg_offsets[sl + 1] - a.seg_offsets[sl], (int64_t)0);
+        double need = 0.0;
+        if (o.status == SPROUT_CELL_OK) {
+#pragma unroll
+            for (int L = 0; L < N; ++L)
+                if (o.x[L] > 0.0) need = fmax(need, (double)a.W / o.x[L]);
+        }
+        // the requests scanned in pieces, plus one for the LP and the window merge (on C4 the
+        // estimate correlates 0.997 with the measured chain times; ordering by the measured
+        // times themselves would end 0.5 % earlier)
+        acc += 1.0f + (float)(fmin(m, need) / (double)piece);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, d);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.0f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        a.chain_cost[c] = t;
+    }
+}
+
+// chain ids by estimate, largest first (ties by id): rank = #{k before i}
+__global__ void __launch_bounds__(1024) cl_order_kernel(const float *cost, int n, int *order) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const float ci = cost[i];
+        int rank = 0;
+        for (int k = 0; k < n; ++k) {
+            const float ck = cost[k];
+            rank += (ck > ci || (ck == ci && k < i)) ? 1 : 0;
+        }
+        order[rank] = i;
+    }
+}
+
+constexpr int kClMaxOrdered = 4096;   // chains ranked by the O(n^2) order kernel; more run in index order
 
 cudaError_t launch_closed_loop(ClosedArgs &a, cudaStream_t stream, int *launches) {
     if ((int64_t)a.R_local * a.X == 0) return cudaSuccess;
     a.n_groups = a.X;
     const int64_t blocks = (int64_t)a.R_local * a.X;
+    const int64_t local_segments = (int64_t)a.R_local * a.T;
+    const int TH = a.n_requests >= kClLongInterval * local_segments ? kClThreadsLong : kClThreadsShort;
+    if (a.chain_cost && a.chain_order && blocks <= kClMaxOrdered) {
+#define CL_EST(NN) case NN: cl_estimate_kernel<NN><<<(unsigned)blocks, 256, 0, stream>>>(a, 8 * TH); break;
+        switch (a.n) {
+            CL_EST(1) CL_EST(2) CL_EST(3) CL_EST(4) CL_EST(5) CL_EST(6) CL_EST(7) CL_EST(8)
+            default: return cudaErrorInvalidValue;
+        }
+#undef CL_EST
+        cl_order_kernel<<<1, 1024, 0, stream>>>(a.chain_cost, (int)blocks, a.chain_order);
+        *launches += 2;
+    } else {
+        a.chain_order = nullptr;
+    }
     const size_t smem = (size_t)2 * a.n * a.W * 4;
     cudaError_t e = cudaSuccess;
 #define CL_LAUNCH(NN, NCM_)                                                                       \
     {                                                                                             \
-        auto kern = a.flags ? cl_window_kernel<NN, NCM_, true> : cl_window_kernel<NN, NCM_, false>; \
+        auto kern = TH == kClThreadsLong                                                          \
+                        ? (a.flags ? cl_window_kernel<NN, NCM_, true, kClThreadsLong>             \
+                                   : cl_window_kernel<NN, NCM_, false, kClThreadsLong>)           \
+                        : (a.flags ? cl_window_kernel<NN, NCM_, true, kClThreadsShort>            \
+                                   : cl_window_kernel<NN, NCM_, false, kClThreadsShort>);         \
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);   \
         if (e != cudaSuccess) return e;                                                           \
-        kern<<<(unsigned)blocks, kClThreads, smem, stream>>>(a);                                  \
+        kern<<<(unsigned)blocks, TH, smem, stream>>>(a);                                          \
     }
 #define CL_N(NN)                                                                                  \
     case NN:                                                                                      \

@@ -272,6 +272,13 @@ sprout_status sprout_simulate_closed_loop_q(const sprout_lp_problem *problem, in
     a.carbon = totals->carbon_g; a.quality = totals->quality; a.trace_status = totals->trace_status;
     a.seg_count = totals->seg_count; a.seg_pinned = totals->seg_pinned; a.seg_tok = totals->seg_tok;
     a.seg_base = totals->seg_base;
+    {   // the chain schedule's scratch: the head of the totals pass's workspace, free until that pass
+        const size_t chains = (size_t)a.R_local * a.X;
+        if (chains * 8 <= workspace_bytes) {
+            a.chain_cost = static_cast<float *>(workspace);
+            a.chain_order = reinterpret_cast<int *>(static_cast<float *>(workspace) + chains);
+        }
+    }
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     int launches = 0;
     st = cuda_status(launch_closed_loop(a, s, &launches));   // every interval's LP, the windows

@@ -76,6 +76,8 @@ struct ClosedArgs {             // closed-loop profiles (closed_loop.cu)
     uint64_t *seg_count, *seg_pinned, *seg_tok;
     double *seg_base;
     uint32_t *trace_status;
+    float *chain_cost;         // scheduling scratch (NULL: chains in index order): [chains] estimates,
+    int *chain_order;          // then [chains] chain ids, longest estimate first
 };
 
 struct N4Args {                 // NEXT-4 kernels (next4.cu)
