@@ -2310,7 +2310,10 @@ bool make_sim_plan(int n, int X, int NC, SimPlan *plan, int max_keys) {
         while (c < M) c <<= 1;
         p.sort_cap = (int)(c < 32 ? 32 : c);
     }
-    if (p.sort_cap > 4096) kcap = -1;     // too many thresholds to merge per warp: generic path
+    if (p.sort_cap > 4096) {              // too many thresholds to merge per warp: generic path
+        kcap = -1;                        // (prep then only marks segments generic: no sort buffer)
+        p.sort_cap = 0;
+    }
     auto per_warp = [&](int kc, int *nb_out, int *kp_out) {
         const int kk = kc < 0 ? 0 : kc;
         const int nb = kk + 3;
@@ -2329,6 +2332,7 @@ bool make_sim_plan(int n, int X, int NC, SimPlan *plan, int max_keys) {
     size_t bytes = per_warp(kcap, &nb, &kp);
     if (kcap >= 0 && bytes > smem_cap) {
         kcap = -1;
+        p.sort_cap = 0;
         bytes = per_warp(kcap, &nb, &kp);
     }
     p.kcap = kcap;

@@ -167,9 +167,8 @@ def test_evaluation_q_and_closed_loop_q(name, kw, dt, grace, sample):
                                             (3, 1, True, 25), (2, 1, False, 2000), (4, 1, True, 700)])
 def test_closed_loop_levels_classes_ragged(n, NC, flags, W):
     """The chain kernel's other template instances (n = 1, n = 8, four
-    classes; two xi chains per CTA with and without flags, X = 3 leaving the
-    last group one chain short) on ragged intervals: empty ones, single
-    requests, and one longer than several scan pieces."""
+    classes, flags with one class, large windows) on ragged intervals: empty
+    ones, single requests, and one longer than several scan pieces."""
     from test_gpu_parity import _custom
     w = _custom(n=n, X=3, NC=NC, flags=flags, N=30_000, T=30, R=2, xi=[0.0, 0.35, 1.0])
     off = w.spec.seg_offsets
@@ -191,3 +190,24 @@ def test_closed_loop_levels_classes_ragged(n, NC, flags, W):
     np.testing.assert_array_equal(got["tok"].reshape(-1, NC, n), want["tok"])
     for k in ("energy", "time", "carbon", "quality"):
         np.testing.assert_allclose(got[k].reshape(-1), want[k], rtol=FP_RTOL, atol=0, err_msg=k)
+
+
+@pytest.mark.parametrize("X,N,T,NC,flags", [(2100, 3000, 4, 1, False), (37, 400_000, 6, 1, False),
+                                             (5, 300_000, 5, 2, True)])
+def test_closed_loop_chain_schedule(X, N, T, NC, flags):
+    """The chain schedule is scheduling only: with more chains than the rank
+    kernel orders (R*X > 4096: index order) and with long intervals (the
+    512-thread chains, longest first), every output still equals the oracle's."""
+    from test_gpu_parity import _custom
+    w = _custom(X=X, R=2, T=T, N=N, NC=NC, flags=flags)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, fl = synth.host_trace(w.spec, sh)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=fl)
+    prof = sw.closed_loop(50, profile=True)
+    torch.cuda.synchronize()
+    got = sw.host()
+    want = oracle.closed_loop(w.prob, w.cost, 50, w.spec.seg_offsets, toks, fl)
+    np.testing.assert_array_equal(prof.cpu().numpy().view(np.uint64), want["profile"].view(np.uint64))
+    np.testing.assert_array_equal(got["x"].view(np.uint64), want["x"].view(np.uint64))
+    np.testing.assert_array_equal(got["cnt"].reshape(want["cnt"].shape), want["cnt"])
+    np.testing.assert_allclose(got["carbon"].reshape(-1), want["carbon"], rtol=FP_RTOL, atol=0)

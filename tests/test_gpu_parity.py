@@ -267,6 +267,24 @@ def test_arbitrary_thresholds_slow_path():
             np.testing.assert_array_equal(cnt[s, j, 0], np.bincount(lv[j, a:b], minlength=4)[:4])
 
 
+@pytest.mark.parametrize("n,X", [(3, 2100), (2, 4096), (3, 4096)])
+def test_large_xi_generic_path(n, X):
+    """Up to SPROUT_MAX_XI xi values: more thresholds per segment than the
+    per-warp breakpoint merge takes (n = 3, X > 2048) run the generic
+    per-cell path, whose prep pass needs no sort buffer; n = 2, X = 4096 is
+    the largest merge.  Cells and totals equal the oracle's."""
+    w = _custom(n=n, X=X, N=6000, T=3, R=1)
+    sh = synth.shard(w.spec, 1, 0)
+    toks, flags = synth.host_trace(w.spec, sh)
+    sw = Sweep(w.prob, w.cost, sh, DEV, tokens=toks, flags=flags)
+    sw.solve()
+    sw.simulate()
+    torch.cuda.synchronize()
+    got = sw.host()
+    compare_cells(got, oracle.solve_cells(w.prob))
+    compare_sim(got, oracle_shard(w, sh, toks, flags), X, 1, n)
+
+
 def test_bad_class_and_bad_offsets_flagged():
     w = _custom(N=5000, T=6, R=1, NC=2, flags=True)
     sh = synth.shard(w.spec, 1, 0)
