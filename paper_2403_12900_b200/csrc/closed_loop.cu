@@ -29,6 +29,7 @@
 // order exactly.  With E = ef + et*tok (reading L11) the window mean is a
 // function of per-class counts and token sums -- exact integers -- so the
 // profile, and the LP decision it feeds, are bit-identical to the oracle's.
+#include <algorithm>
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "sprout_device.cuh"
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 2) cl_window_kernel(const 
     const int chain = a.chain_order ? a.chain_order[blockIdx.x] : (int)blockIdx.x;   // longest first
     const int rl = chain / a.X, j = chain % a.X;
 #if SPROUT_CL_TIMING_PRINT
+    long long cyc_lp = 0, cyc_scan = 0, cyc_merge = 0;
     unsigned long long t_start;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
@@ -199,6 +201,9 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 2) cl_window_kernel(const 
         const int64_t c00 = e_al - kClPiece + 8 * (int64_t)tid;
         const bool any0 = s0 <= s1 && c00 + 8 > s0 && c00 < s1 && s1 <= a.n_requests && s0 >= 0;
         if (warp != 0) load_chunk<N, FLAGS>(a, c00, any0, ch);
+#if SPROUT_CL_TIMING_PRINT
+        long long ph0 = clock64();
+#endif
         // ---- the interval's LP with the closed-loop profile ----
         if (tid == 0) {
             const int64_t cell = sl * a.X + j;
@@ -267,10 +272,16 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 2) cl_window_kernel(const 
         if (tid < N) seen[tid] = 0u;
         __syncthreads();
         const bool run = seg_ok_s && ok_s;
+#if SPROUT_CL_TIMING_PRINT
+        long long ph1 = clock64();
+#endif
         uint32_t T[N > 1 ? N - 1 : 1];
 #pragma unroll
         for (int i = 0; i + 1 < N; ++i) T[i] = thr_s[i];
         const int ml = ml_s;
+        uint32_t thr_on[N > 1 ? N - 1 : 1];   // thresholds below the max level count
+#pragma unroll
+        for (int i = 0; i + 1 < N; ++i) thr_on[i] = i < ml ? 0xFFu : 0u;
         // ---- backward scan: the interval's last W requests of every reachable level ----
         if (run) {
             if (warp == 0) load_chunk<N, FLAGS>(a, c00, any0, ch);
@@ -288,22 +299,40 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 2) cl_window_kernel(const 
                     const int64_t lo = min(max(s0 - c0, (int64_t)0), (int64_t)8), hi = min(max(s1 - c0, (int64_t)0), (int64_t)8);
                     valid = ((1u << (uint32_t)hi) - 1u) & ~((1u << (uint32_t)lo) - 1u);
                 }
-                uint32_t lv = 0u;
-                uint64_t pk = 0ull;   // per-level counts of the chunk, one byte per level
+                // the chunk's requests of each level as bit masks: ge_i = {k : w_k >= T_i} over
+                // the thresholds below the interval's max level -- an OK cell's thresholds are
+                // non-decreasing, so #{i < ml : w >= T_i} = min(#{i : w >= T_i}, ml), the a6
+                // level -- with opted-out requests at level 0
+                uint32_t ge[N > 1 ? N - 1 : 1], pin = 0u;
+#pragma unroll
+                for (int i = 0; i + 1 < N; ++i) ge[i] = 0u;
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
-                    const uint32_t fb = flag_byte(ch.fw, k);
-                    if (FLAGS && ((fb >> 1) & 3u) >= (uint32_t)NC) valid &= ~(1u << k);
-                    const int L = cl_level<N>(ch.w[k], T, ml, FLAGS && (fb & 1u));
-                    lv |= (uint32_t)L << (4 * k);
-                    pk += ((valid >> k) & 1u) ? (1ull << (8 * L)) : 0ull;
+                    if (FLAGS) {
+                        const uint32_t fb = flag_byte(ch.fw, k);
+                        if (((fb >> 1) & 3u) >= (uint32_t)NC) valid &= ~(1u << k);
+                        pin |= (fb & 1u) << k;
+                    }
+#pragma unroll
+                    for (int i = 0; i + 1 < N; ++i) ge[i] |= (ch.w[k] >= T[i] ? 1u : 0u) << k;
+                }
+                uint32_t lm[N];   // valid requests of level L
+                {
+                    uint32_t below = valid;   // valid requests not yet placed at a lower level
+#pragma unroll
+                    for (int L = 0; L + 1 < N; ++L) {
+                        const uint32_t up = ge[L] & thr_on[L] & ~pin;
+                        lm[L] = below & ~up;
+                        below &= up;
+                    }
+                    lm[N - 1] = below;
                 }
                 // requests of each level in LATER threads of the warp (suffix scan)
                 uint32_t after[N];
                 uint32_t (*wt)[N] = wtot[pi & 1];
 #pragma unroll
                 for (int L = 0; L < N; ++L) {
-                    const uint32_t c = (uint32_t)(pk >> (8 * L)) & 0xFFu;
+                    const uint32_t c = (uint32_t)__popc(lm[L]);
                     uint32_t x = c;
 #pragma unroll
                     for (int d = 1; d < 32; d <<= 1) {
@@ -331,21 +360,16 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 2) cl_window_kernel(const 
                 const bool done = __all_sync(0xFFFFFFFFu, lane >= N || !((act_s >> lane) & 1) || seen_r >= (uint32_t)W);
                 // the thread's requests from the latest: reverse rank = level-L requests after it;
                 // only levels whose window is not yet full need ranks
-                uint32_t need = 0u;
 #pragma unroll
-                for (int L = 0; L < N; ++L) need |= (after[L] < (uint32_t)W) ? (1u << L) : 0u;
-                if (valid && need) {
+                for (int L = 0; L < N; ++L) {
+                    if (after[L] >= (uint32_t)W || !lm[L]) continue;
 #pragma unroll
                     for (int k = 7; k >= 0; --k) {
-                        if (!((valid >> k) & 1u)) continue;
-                        const int L = (int)((lv >> (4 * k)) & 15u);
-                        if (!((need >> L) & 1u)) continue;
-                        uint32_t rho = 0u, tl = 0u;
-#pragma unroll
-                        for (int LL = 0; LL < N; ++LL)
-                            if (LL == L) { rho = after[LL]; after[LL] += 1u; tl = cl_half(ch.tk[LL], k); }
+                        if (!((lm[L] >> k) & 1u)) continue;
+                        const uint32_t rho = after[L]++;
                         if (rho < (uint32_t)W)
-                            scr[(size_t)L * W + rho] = (FLAGS ? (((flag_byte(ch.fw, k) >> 1) & 3u) << 16) : 0u) | tl;
+                            scr[(size_t)L * W + rho] =
+                                (FLAGS ? (((flag_byte(ch.fw, k) >> 1) & 3u) << 16) : 0u) | cl_half(ch.tk[L], k);
                     }
                 }
                 if (done) break;
@@ -353,6 +377,9 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 2) cl_window_kernel(const 
             if (warp == 0 && lane < N) seen[lane] = seen_r;
             __syncthreads();   // every scratch entry written, seen final
         }
+#if SPROUT_CL_TIMING_PRINT
+        long long ph2 = clock64();
+#endif
         // ---- append the scratch entries (forward order) to the rings, evicting the oldest ----
         int dn[N][NCM], dk[N][NCM];
 #pragma unroll
@@ -419,12 +446,17 @@ __global__ void __launch_bounds__(TH, TH >= 512 ? 1 : 2) cl_window_kernel(const 
             size[tid] = (int)min(sz + k, (uint32_t)W);
         }
         __syncthreads();
+#if SPROUT_CL_TIMING_PRINT
+        const long long ph3 = clock64();
+        cyc_lp += ph1 - ph0; cyc_scan += ph2 - ph1; cyc_merge += ph3 - ph2;
+#endif
     }
 #if SPROUT_CL_TIMING_PRINT
     if (tid == 0) {
         unsigned long long t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        printf("CHAIN %d %d %d %.3f %.3f\n", (int)blockIdx.x, rl, j, t_start * 1e-6, (t_end - t_start) * 1e-6);
+        printf("CHAIN %d %d %d %.3f %.3f %lld %lld %lld\n", (int)blockIdx.x, rl, j, t_start * 1e-6, (t_end - t_start) * 1e-6,
+               cyc_lp, cyc_scan, cyc_merge);
     }
 #endif
 }
@@ -460,10 +492,10 @@ __global__ void __launch_bounds__(256) cl_estimate_kernel(const __grid_constant_
             for (int L = 0; L < N; ++L)
                 if (o.x[L] > 0.0) need = fmax(need, (double)a.W / o.x[L]);
         }
-        // the requests scanned in pieces, plus one for the LP and the window merge (on C4 the
-        // estimate correlates 0.997 with the measured chain times; ordering by the measured
-        // times themselves would end 0.5 % earlier)
-        acc += 1.0f + (float)(fmin(m, need) / (double)piece);
+        // the requests scanned, in pieces, plus the interval's fixed part (LP, window merge,
+        // barriers), which costs about 1.9 pieces' time (C4, per-chain phase timing:
+        // 4.1 us per interval + 2.2 us per 4,096 requests scanned)
+        acc += 1.9f + (float)(fmin(m, need) / (double)piece);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, d);
@@ -476,20 +508,113 @@ __global__ void __launch_bounds__(256) cl_estimate_kernel(const __grid_constant_
     }
 }
 
-// chain ids by estimate, largest first (ties by id): rank = #{k before i}
-__global__ void __launch_bounds__(1024) cl_order_kernel(const float *cost, int n, int *order) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const float ci = cost[i];
+// The launch order.  The block scheduler hands each freed slot (SMs x CTAs per
+// SM) the next chain in launch order, i.e. list scheduling; longest-first
+// list scheduling leaves the short chains to start last on busy slots.  So:
+// MULTIFIT -- binary search of a capacity C for which first-fit-decreasing
+// packs the chains into `slots` bins -- and then the chains in the order of
+// their planned start times, which list scheduling reproduces when the
+// estimates hold (each freed slot is the one whose chain was planned to end
+// first).  No capacity packs (cannot happen for C >= sum / slots + max, the
+// search's upper end): longest first.  One CTA; the first-fit scan is one
+// warp, each lane holding every 32nd bin's load.
+constexpr int kClMaxOrdered = 4000;   // chains scheduled (48 KB of static shared memory); more run in index order
+constexpr int kClMaxSlots = 32 * 32;  // bins of the first-fit scan (32 per lane)
+
+__global__ void __launch_bounds__(1024) cl_order_kernel(const float *cost, int n, int slots, int *order) {
+    __shared__ float e[kClMaxOrdered], start[kClMaxOrdered];
+    __shared__ int byc[kClMaxOrdered];   // chain ids by estimate, largest first
+    __shared__ float bound[2];
+    __shared__ int feasible;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < n; i += blockDim.x) e[i] = cost[i];
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {   // rank: larger first, ties by id
+        const float ci = e[i];
+        int rank = 0;
+        for (int k = 0; k < n; ++k) rank += (e[k] > ci || (e[k] == ci && k < i)) ? 1 : 0;
+        byc[rank] = i;
+    }
+    if (tid == 0) {
+        float sum = 0.0f, mx = 0.0f;
+        for (int i = 0; i < n; ++i) { sum += e[i]; mx = fmaxf(mx, e[i]); }
+        bound[0] = fmaxf(mx, sum / (float)slots);           // no schedule is shorter
+        bound[1] = sum / (float)slots + mx;                  // list scheduling reaches this
+        feasible = 0;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        float lo = bound[0], hi = bound[1];
+        bool have = false;
+        for (int it = 0; it < 14; ++it) {
+            const float C = (it == 0) ? hi : 0.5f * (lo + hi);
+            float load[kClMaxSlots / 32];
+#pragma unroll
+            for (int b = 0; b < kClMaxSlots / 32; ++b) load[b] = 0.0f;
+            bool ok = true;
+            for (int q = 0; q < n && ok; ++q) {
+                const int c = byc[q];
+                const float ec = e[c];
+                int first = -1;   // the first bin (index b * 32 + lane) the chain fits in
+#pragma unroll
+                for (int b = 0; b < kClMaxSlots / 32; ++b) {
+                    const bool fits = b * 32 + lane < slots && load[b] + ec <= C;
+                    const unsigned bal = __ballot_sync(0xFFFFFFFFu, fits);
+                    if (first < 0 && bal) first = b * 32 + __ffs(bal) - 1;
+                }
+                if (first < 0) {
+                    ok = false;
+                } else if ((first & 31) == lane) {
+#pragma unroll
+                    for (int b = 0; b < kClMaxSlots / 32; ++b)
+                        if (b == (first >> 5)) { start[c] = load[b]; load[b] += ec; }
+                }
+            }
+            if (ok) { hi = C; have = true; } else { lo = C; }
+            if (it > 0 && hi - lo <= 1e-3f * hi) break;
+        }
+        // the starts of the final (smallest feasible) capacity
+        if (have) {
+            float load[kClMaxSlots / 32];
+#pragma unroll
+            for (int b = 0; b < kClMaxSlots / 32; ++b) load[b] = 0.0f;
+            for (int q = 0; q < n; ++q) {
+                const int c = byc[q];
+                const float ec = e[c];
+                int first = -1;
+#pragma unroll
+                for (int b = 0; b < kClMaxSlots / 32; ++b) {
+                    const bool fits = b * 32 + lane < slots && load[b] + ec <= hi;
+                    const unsigned bal = __ballot_sync(0xFFFFFFFFu, fits);
+                    if (first < 0 && bal) first = b * 32 + __ffs(bal) - 1;
+                }
+                if (first >= 0 && (first & 31) == lane) {
+#pragma unroll
+                    for (int b = 0; b < kClMaxSlots / 32; ++b)
+                        if (b == (first >> 5)) { start[c] = load[b]; load[b] += ec; }
+                }
+                if (first < 0) have = false;
+            }
+        }
+        if (lane == 0) feasible = have ? 1 : 0;
+    }
+    __syncthreads();
+    if (!feasible) {
+        for (int i = tid; i < n; i += blockDim.x) order[i] = byc[i];
+        return;
+    }
+    for (int i = tid; i < n; i += blockDim.x) {   // by planned start, ties: larger estimate first
+        const int ci = byc[i];
+        const float si = start[ci];
         int rank = 0;
         for (int k = 0; k < n; ++k) {
-            const float ck = cost[k];
-            rank += (ck > ci || (ck == ci && k < i)) ? 1 : 0;
+            const float sk = start[byc[k]];
+            rank += (sk < si || (sk == si && k < i)) ? 1 : 0;
         }
-        order[rank] = i;
+        order[rank] = ci;
     }
 }
 
-constexpr int kClMaxOrdered = 4096;   // chains ranked by the O(n^2) order kernel; more run in index order
 
 cudaError_t launch_closed_loop(ClosedArgs &a, cudaStream_t stream, int *launches) {
     if ((int64_t)a.R_local * a.X == 0) return cudaSuccess;
@@ -504,7 +629,27 @@ cudaError_t launch_closed_loop(ClosedArgs &a, cudaStream_t stream, int *launches
             default: return cudaErrorInvalidValue;
         }
 #undef CL_EST
-        cl_order_kernel<<<1, 1024, 0, stream>>>(a.chain_cost, (int)blocks, a.chain_order);
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+        const size_t smem_chain = (size_t)2 * a.n * a.W * 4;
+#define CL_OCC(NN)                                                                                \
+    case NN:                                                                                      \
+        e = TH == kClThreadsLong                                                                  \
+                ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                  \
+                      &per_sm, cl_window_kernel<NN, 1, false, kClThreadsLong>, TH, smem_chain)    \
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(                                  \
+                      &per_sm, cl_window_kernel<NN, 1, false, kClThreadsShort>, TH, smem_chain);  \
+        break;
+        switch (a.n) {
+            CL_OCC(1) CL_OCC(2) CL_OCC(3) CL_OCC(4) CL_OCC(5) CL_OCC(6) CL_OCC(7) CL_OCC(8)
+            default: return cudaErrorInvalidValue;
+        }
+#undef CL_OCC
+        if (e != cudaSuccess) return e;
+        const int slots = std::min(std::max(sms * std::max(per_sm, 1), 1), kClMaxSlots);
+        cl_order_kernel<<<1, 1024, 0, stream>>>(a.chain_cost, (int)blocks, slots, a.chain_order);
         *launches += 2;
     } else {
         a.chain_order = nullptr;

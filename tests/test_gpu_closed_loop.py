@@ -196,7 +196,7 @@ def test_closed_loop_levels_classes_ragged(n, NC, flags, W):
                                              (5, 300_000, 5, 2, True)])
 def test_closed_loop_chain_schedule(X, N, T, NC, flags):
     """The chain schedule is scheduling only: with more chains than the rank
-    kernel orders (R*X > 4096: index order) and with long intervals (the
+    kernel orders (R*X > 4000: index order) and with long intervals (the
     512-thread chains, longest first), every output still equals the oracle's."""
     from test_gpu_parity import _custom
     w = _custom(X=X, R=2, T=T, N=N, NC=NC, flags=flags)
