@@ -392,9 +392,9 @@ sprout_status sprout_cell_totals_fp64(const sprout_lp_problem *problem, const sp
  * streaming kernel of sprout_simulate_trace accounts every request with the
  * solved thresholds.  `workspace` (device, 256-byte aligned, caller-owned,
  * >= sprout_workspace_bytes) is that pass's; before it, its first 8 bytes
- * per chain hold the chain schedule (an estimate of each chain's scan work
- * from the LP on the priors, and the chains' launch order, longest first --
- * scheduling only: no output depends on it).  Requires whole regions
+ * per chain hold the chain schedule (an estimate of each chain's time from
+ * the LP on the priors, and the launch order that packs the chains into the
+ * GPU's resident slots -- scheduling only: no output depends on it).  Requires whole regions
  * (first_segment and n_segments multiples of n_intervals: a rank may take a
  * range of regions; outputs are indexed by local cell), profile_per_interval
  * 0, and 1 <= window <= 4096 with n*window*4 bytes <= 96 KiB.  Errors:

@@ -9,10 +9,11 @@
 //
 // Chains cost very different times (an interval is scanned back until every
 // level its mix reaches has W requests, so a level with a small share makes
-// the scan deep): two small kernels first estimate each chain's scan work
-// from the LP on the priors and order the chains longest first, so a long
-// chain does not start last.  A chain gets 512 threads (one CTA per SM) when
-// the intervals are long, 256 otherwise.
+// the scan deep): two small kernels first estimate each chain's time from
+// the LP on the priors and plan the launch order (MULTIFIT packing of the
+// chains into the resident slots, then planned start order), so long chains
+// do not start last.  A chain gets 512 threads (one CTA per SM) when the
+// intervals are long, 256 otherwise.
 //
 // A chain is sequential in time by definition, but only the LP decisions and
 // the windows are: once every interval's thresholds are known, the cell
